@@ -1,0 +1,142 @@
+// Shared definitions for the otfx sm_100a kernels.
+//
+// Device layout ("planes"): every real degree of freedom of a per-cell payload
+// lives in its own row-major plane of (rows_alloc x pitch) elements.  A slab
+// that owns global rows [row_begin,row_end) stores local row 0 = ghost row
+// row_begin-1, local rows 1..rows = owned rows, local row rows+1 = ghost row
+// row_end.  Columns are never split, so a warp always reads 32 consecutive
+// elements of one plane row (fully coalesced).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace otfx {
+
+// norm families, numbered as in include/otfx.h
+enum NormId : int { NORM_L2 = 0, NORM_L12 = 1, NORM_L1 = 2, NORM_L1NUC = 3 };
+
+// payload kinds
+enum KindId : int { KIND_SCALAR = 0, KIND_VECTOR = 1, KIND_MATRIX_REAL = 2, KIND_MATRIX_COMPLEX = 3 };
+
+// raw check scalars (per slab; summed / maxed across slabs)
+enum RawId : int {
+  R_PU = 0,     // sum of per-cell norm_u(u)
+  R_PW,         // sum of per-cell norm_w(w)
+  R_SU2,        // sum |u|^2  (eps_reg objective term)
+  R_SW2,        // sum |w|^2
+  R_SCON,       // sum |div u + div_c w - diff|^2
+  R_SPHID,      // <phi, diff>
+  R_PENU,       // sum over u dual blocks of (g-1)_+^2
+  R_PENW,       // sum over w dual blocks of (g-alpha)_+^2
+  R_SDU,        // |u_new - u_old|^2
+  R_SDW,        // |w_new - w_old|^2
+  R_SDPHI,      // |phi_new - phi_old|^2
+  R_SCROSS,     // <dphi, div du + div_c dw>
+  R_NSUM,       // --- number of summed entries
+  R_GU = R_NSUM,  // max u dual-block norm
+  R_GW,           // max w dual-block norm
+  R_NRAW
+};
+
+constexpr int MAX_CHAN_COEF = 2 * 8 * 4 * 4;  // ell<=8 complex 4x4 matrices (re,im)
+
+// Kernel arguments shared by every payload policy.  Passed by value
+// (__grid_constant__) so several engines can run concurrently.
+template <typename T>
+struct StateView {
+  T* u;    // 2*NP planes: x components then y components
+  T* w;    // NW planes
+  T* phi;  // NP planes
+};
+
+template <typename T>
+struct SweepArgs {
+  StateView<T> a;        // read (iterate k)
+  StateView<T> b;        // written (iterate k+1)
+  const T* diff;         // NP planes
+  int64_t plane;         // elements between planes
+  int pitch;             // elements between rows
+  int n;                 // global grid side
+  int row_begin;         // first owned global row
+  int row_end;           // one past the last owned global row
+  int rows_per_block;    // sweep length of one CTA
+  int ell;               // active channel count (edges / Lindblad matrices)
+  int norm_u, norm_w;
+  T mu, thr_w, tau, nu, inv_dx;
+  T den_u, den_w;        // (1 + 2 mu eps), (1 + 2 thr_w eps/alpha); 1 when eps == 0
+  int has_eps;
+  double alpha, eps;
+  double* partials;      // [gridDim.x*gridDim.y][R_NSUM] (CHECK sweeps / evaluate)
+  double* maxes;         // [gridDim.x*gridDim.y][2]
+  double coef[MAX_CHAN_COEF];  // graph D/c (k x ell, row-major) or Lindblad (ell,k,k,{re,im})
+};
+
+template <typename T>
+__device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+
+// IEEE helpers that the parity build relies on (no contraction is done
+// anyway because everything is compiled with --fmad=false).
+template <typename T> __device__ __forceinline__ T tiny_of();
+template <> __device__ __forceinline__ double tiny_of<double>() { return 2.2250738585072014e-308; }
+// float64 tiny cast to float32 underflows to 0 in the reference's fp32 runs
+template <> __device__ __forceinline__ float tiny_of<float>() { return 0.0f; }
+
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+
+template <typename T>
+__device__ __forceinline__ T maxT(T a, T b) {
+  // np.maximum semantics for the finite / inf values that occur here
+  return a > b ? a : b;
+}
+
+// warp + block reduction of NS doubles; result valid in thread 0
+template <int NS>
+__device__ __forceinline__ void block_sum(double (&v)[NS], double* smem /*[32*NS]*/) {
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[s] += __shfl_down_sync(0xffffffffu, v[s], o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) smem[wid * NS + s] = v[s];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      double acc = 0.0;
+      for (int q = 0; q < nw; ++q) acc += smem[q * NS + s];
+      v[s] = acc;
+    }
+  }
+}
+
+template <int NS>
+__device__ __forceinline__ void block_max(double (&v)[NS], double* smem) {
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[s] = dmax(v[s], __shfl_down_sync(0xffffffffu, v[s], o));
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) smem[wid * NS + s] = v[s];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      double acc = smem[s];
+      for (int q = 1; q < nw; ++q) acc = dmax(acc, smem[q * NS + s]);
+      v[s] = acc;
+    }
+  }
+}
+
+}  // namespace otfx

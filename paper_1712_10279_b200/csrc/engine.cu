@@ -1,0 +1,1267 @@
+// Host runtime of the otfx engine: device memory, layout conversion, the
+// iteration / check / run loops (CUDA graphs), halo exchange (local copies or
+// NCCL over NVLink), and the extern "C" ABI of include/otfx.h.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/otfx.h"
+#include "ops.h"
+
+namespace otfx {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      throw Error(e_ == cudaErrorMemoryAllocation ? OTFX_ENOMEM : OTFX_ECUDA,                 \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+  } while (0)
+
+static void require(bool ok, int code, const std::string& msg) {
+  if (!ok) throw Error(code, msg);
+}
+
+template <>
+const Ops<double>* find_ops<double>(int kind, int K) {
+  if (kind == KIND_SCALAR) return ops_vector_f64(1, false);
+  if (kind == KIND_VECTOR) return ops_vector_f64(K, true);
+  return ops_matrix_f64(kind, K);
+}
+template <>
+const Ops<float>* find_ops<float>(int kind, int K) {
+  if (kind == KIND_SCALAR) return ops_vector_f32(1, false);
+  if (kind == KIND_VECTOR) return ops_vector_f32(K, true);
+  return ops_matrix_f32(kind, K);
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time so the library has no hard NCCL dependency
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  if (api.h) return api;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char* nm : names) {
+    api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (api.h) break;
+  }
+  require(api.h != nullptr, OTFX_ENCCL, "NCCL library (libnccl.so.2) not found");
+#define SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(api.h, name))
+  SYM(GetUniqueId, "ncclGetUniqueId");
+  SYM(CommInitRank, "ncclCommInitRank");
+  SYM(CommDestroy, "ncclCommDestroy");
+  SYM(Send, "ncclSend");
+  SYM(Recv, "ncclRecv");
+  SYM(AllReduce, "ncclAllReduce");
+  SYM(GroupStart, "ncclGroupStart");
+  SYM(GroupEnd, "ncclGroupEnd");
+  SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+  require(api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.AllReduce &&
+              api.GroupStart && api.GroupEnd,
+          OTFX_ENCCL, "NCCL library lacks required symbols");
+  return api;
+}
+
+#define NK(call)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      throw Error(OTFX_ENCCL, std::string(#call) + ": " +                               \
+                                  (nccl().GetErrorString ? nccl().GetErrorString(r_) : "")); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// layout conversion kernels (reference AoS <-> device planes)
+// ---------------------------------------------------------------------------
+constexpr int MAXMAP = 256;
+
+struct PackMap {
+  int np;                 // planes written
+  int rec;                // doubles per cell record in the source
+  int src[MAXMAP];        // record index per plane (-1: zero)
+  double wt[MAXMAP];      // plane weight for the sum of squares
+  int nmass;              // record indices summed into the mass
+  int mass[16];
+};
+
+struct UnpackMap {
+  int rec;                // doubles per cell record in the destination
+  int plane[MAXMAP];      // source plane per record element (-1: zero)
+  signed char sign[MAXMAP];
+};
+
+// planes[p] = T(src0[rec*cell + map] (- src1[...])), rows [0, nrows) of the chunk
+// written to local rows lrow0 + r.  Per-block partials: mass0, mass1, sumsq.
+template <typename T>
+__global__ void pack_kernel(const double* __restrict__ s0, const double* __restrict__ s1,
+                            int64_t ncell, int n, T* planes, int64_t plane, int pitch, int lrow0,
+                            const __grid_constant__ PackMap m, double* part) {
+  __shared__ double sred[32 * 3];
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < ncell;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(c / n), j = int(c % n);
+    const double* a = s0 + c * m.rec;
+    const double* b = s1 ? s1 + c * m.rec : nullptr;
+    const int64_t o = int64_t(lrow0 + r) * pitch + j;
+    for (int p = 0; p < m.np; ++p) {
+      double v = 0.0;
+      if (m.src[p] >= 0) v = b ? (a[m.src[p]] - b[m.src[p]]) : a[m.src[p]];
+      planes[p * plane + o] = T(v);
+      acc[2] += m.wt[p] * v * v;
+    }
+    for (int q = 0; q < m.nmass; ++q) {
+      acc[0] += a[m.mass[q]];
+      if (b) acc[1] += b[m.mass[q]];
+    }
+  }
+  block_sum<3>(acc, sred);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 3 + 0] = acc[0];
+    part[blockIdx.x * 3 + 1] = acc[1];
+    part[blockIdx.x * 3 + 2] = acc[2];
+  }
+}
+
+template <typename T>
+__global__ void unpack_kernel(const T* __restrict__ planes, int64_t plane, int pitch, int lrow0,
+                              int64_t ncell, int n, const __grid_constant__ UnpackMap m,
+                              double* dst) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < ncell;
+       c += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(c / n), j = int(c % n);
+    const int64_t o = int64_t(lrow0 + r) * pitch + j;
+    double* d = dst + c * m.rec;
+    for (int q = 0; q < m.rec; ++q) {
+      const int p = m.plane[q];
+      d[q] = p >= 0 ? double(m.sign[q]) * double(planes[p * plane + o]) : 0.0;
+    }
+  }
+}
+
+// Deterministic final reduction of the per-block partials into raw[OTFX_NRAW].
+__global__ void reduce_raw_kernel(const double* __restrict__ pe, const double* __restrict__ me,
+                                  int nbe, const double* __restrict__ ps, int nbs, int with_res,
+                                  double* raw) {
+  __shared__ double sred[32 * 14];
+  double v[14];
+  for (int q = 0; q < 14; ++q) v[q] = 0.0;
+  for (int b = threadIdx.x; b < nbe; b += blockDim.x) {
+    for (int q = 0; q < 8; ++q) v[q] += pe[b * 8 + q];
+  }
+  if (with_res) {
+    for (int b = threadIdx.x; b < nbs; b += blockDim.x) {
+      for (int q = 0; q < 4; ++q) v[8 + q] += ps[b * 4 + q];
+    }
+  }
+  double mx[2] = {0.0, 0.0};
+  for (int b = threadIdx.x; b < nbe; b += blockDim.x) {
+    mx[0] = dmax(mx[0], me[b * 2]);
+    mx[1] = dmax(mx[1], me[b * 2 + 1]);
+  }
+  double s12[12];
+  for (int q = 0; q < 12; ++q) s12[q] = v[q];
+  block_sum<12>(s12, sred);
+  block_max<2>(mx, sred);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 12; ++q) raw[q] = s12[q];
+    raw[R_GU] = mx[0];
+    raw[R_GW] = mx[1];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the engine
+// ---------------------------------------------------------------------------
+constexpr int kPackBlocks = 296;
+
+struct EngineBase {
+  virtual ~EngineBase() {}
+};
+
+}  // namespace otfx
+
+struct otfx_engine {
+  otfx_engine_desc d{};
+  std::vector<double> chan;
+  int elem = 8;
+  int K = 1, NP = 1, NWS = 0, LMAX = 0, NWact = 0;
+  bool has_w = false;
+  int rows = 0, rows_alloc = 0, pitch = 0;
+  int64_t plane = 0;
+  size_t state_bytes = 0, total_bytes = 0;
+  unsigned char* mem = nullptr;
+  void* u[2]{};
+  void* w[2]{};
+  void* phi[2]{};
+  void* diff = nullptr;
+  int cur = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // sweep geometry
+  int TX = 128, R = 64, gx = 1, gy = 1;
+  size_t smem_plain = 0, smem_check = 0;
+  // reductions
+  double* d_part_sweep = nullptr;  // [gx*gy][4]
+  double* d_part_eval = nullptr;   // [ex*ey][8]
+  double* d_max_eval = nullptr;    // [ex*ey][2]
+  double* d_raw = nullptr;         // [OTFX_NRAW]
+  double* h_raw = nullptr;         // pinned
+  int ex = 1, ey = 1;
+  bool residual_valid = false;
+  double diff_norm = 0.0;
+  // staging for host <-> device conversions
+  double* d_stage = nullptr;
+  size_t stage_bytes = 0;
+  double* d_pack_part = nullptr;
+  double* h_pack_part = nullptr;
+  // graphs
+  bool use_graphs = true;
+  std::map<std::pair<int, int64_t>, cudaGraphExec_t> graphs;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  void* d_halo = nullptr;  // send/recv buffers
+  // policy dispatch
+  const otfx::Ops<double>* ops64 = nullptr;
+  const otfx::Ops<float>* ops32 = nullptr;
+};
+
+namespace otfx {
+
+static int pair_index_rt(int K, int a, int b) { return a * K - a * (a + 1) / 2 + (b - a - 1); }
+
+template <typename T>
+static SweepArgs<T> make_args(otfx_engine* e, int from) {
+  SweepArgs<T> a;
+  memset(&a, 0, sizeof(a));
+  const int to = from ^ 1;
+  a.a = {static_cast<T*>(e->u[from]), static_cast<T*>(e->w[from]), static_cast<T*>(e->phi[from])};
+  a.b = {static_cast<T*>(e->u[to]), static_cast<T*>(e->w[to]), static_cast<T*>(e->phi[to])};
+  a.diff = static_cast<const T*>(e->diff);
+  a.plane = e->plane;
+  a.pitch = e->pitch;
+  a.n = e->d.n;
+  a.row_begin = e->d.row_begin;
+  a.row_end = e->d.row_end;
+  a.rows_per_block = e->R;
+  a.ell = e->d.ell;
+  a.norm_u = e->d.norm_u;
+  a.norm_w = e->d.norm_w;
+  const double mu = e->d.mu, nu = e->d.nu, alpha = e->d.alpha, eps = e->d.eps_reg;
+  const double thr_w = alpha * nu;  // S/solver.py:213
+  a.mu = T(mu);
+  a.nu = T(nu);
+  a.thr_w = T(thr_w);
+  a.tau = T(e->d.tau);
+  a.inv_dx = T(e->d.inv_dx);
+  a.has_eps = eps > 0 ? 1 : 0;
+  // S/shrink.py:240 divides by (1 + 2 mu eps); w uses eps/alpha (S/solver.py:215-217)
+  a.den_u = T(eps > 0 ? 1.0 + 2.0 * mu * eps : 1.0);
+  a.den_w = T(eps > 0 ? 1.0 + 2.0 * thr_w * (eps / alpha) : 1.0);
+  a.alpha = alpha;
+  a.eps = eps;
+  a.partials = e->d_part_sweep;
+  a.maxes = nullptr;
+  const int K = e->K;
+  if (e->d.kind == OTFX_KIND_VECTOR) {
+    const int L = e->LMAX;
+    for (int c = 0; c < K; ++c)
+      for (int q = 0; q < e->d.ell; ++q) a.coef[c * L + q] = e->chan[size_t(c) * e->d.ell + q];
+  } else if (e->d.kind != OTFX_KIND_SCALAR) {
+    for (size_t q = 0; q < e->chan.size(); ++q) a.coef[q] = e->chan[q];
+  }
+  return a;
+}
+
+template <typename T>
+static const Ops<T>* ops_of(otfx_engine* e);
+template <>
+const Ops<double>* ops_of<double>(otfx_engine* e) { return e->ops64; }
+template <>
+const Ops<float>* ops_of<float>(otfx_engine* e) { return e->ops32; }
+
+template <typename T>
+static void launch_sweep(otfx_engine* e, bool check) {
+  SweepArgs<T> a = make_args<T>(e, e->cur);
+  CK(ops_of<T>(e)->sweep(a, dim3(e->gx, e->gy), dim3(e->TX), check ? e->smem_check : e->smem_plain,
+                         e->stream, check));
+  e->cur ^= 1;
+}
+
+static void launch_sweep(otfx_engine* e, bool check) {
+  if (e->elem == 8) launch_sweep<double>(e, check);
+  else launch_sweep<float>(e, check);
+}
+
+template <typename T>
+static void launch_evaluate(otfx_engine* e) {
+  SweepArgs<T> a = make_args<T>(e, e->cur);
+  a.partials = e->d_part_eval;
+  a.maxes = e->d_max_eval;
+  CK(ops_of<T>(e)->evaluate(a, dim3(e->ex, e->ey), dim3(128), e->stream));
+}
+
+static void launch_evaluate(otfx_engine* e) {
+  if (e->elem == 8) launch_evaluate<double>(e);
+  else launch_evaluate<float>(e);
+}
+
+// halo rows: top ghost (local 0) <- previous slab's last row (phi + u);
+// bottom ghost (local rows+1) <- next slab's first row (phi)
+static void copy_rows(otfx_engine* dst, void* dbase, int drow, otfx_engine* src, void* sbase,
+                      int srow, int nplanes, cudaStream_t s) {
+  // plane strides differ between slabs of different heights
+  const size_t w = size_t(dst->d.n) * dst->elem;
+  const size_t dpb = size_t(dst->plane) * dst->elem, spb = size_t(src->plane) * src->elem;
+  CK(cudaMemcpy2DAsync(static_cast<char*>(dbase) + size_t(drow) * dst->pitch * dst->elem, dpb,
+                       static_cast<char*>(sbase) + size_t(srow) * src->pitch * src->elem, spb, w,
+                       nplanes, cudaMemcpyDeviceToDevice, s));
+}
+
+static void exchange_nccl(otfx_engine* e) {
+  if (!e->comm || e->nranks == 1) return;
+  NcclApi& N = nccl();
+  const int c = e->cur;
+  const size_t w = size_t(e->d.n);
+  const size_t pb = size_t(e->plane) * e->elem;
+  const size_t wb = w * e->elem;
+  const int NP = e->NP;
+  char* buf = static_cast<char*>(e->d_halo);
+  char* send_top = buf;                       // NP rows: phi(first row) -> rank-1
+  char* send_bot = send_top + NP * wb;        // 3NP rows: phi, u (last row) -> rank+1
+  char* recv_top = send_bot + 3 * NP * wb;    // 3NP rows from rank-1
+  char* recv_bot = recv_top + 3 * NP * wb;    // NP rows from rank+1
+  auto rowp = [&](void* base, int lrow) {
+    return static_cast<char*>(base) + size_t(lrow) * e->pitch * e->elem;
+  };
+  const bool has_prev = e->rank > 0, has_next = e->rank + 1 < e->nranks;
+  if (has_prev) CK(cudaMemcpy2DAsync(send_top, wb, rowp(e->phi[c], 1), pb, wb, NP, cudaMemcpyDeviceToDevice, e->stream));
+  if (has_next) {
+    CK(cudaMemcpy2DAsync(send_bot, wb, rowp(e->phi[c], e->rows), pb, wb, NP, cudaMemcpyDeviceToDevice, e->stream));
+    CK(cudaMemcpy2DAsync(send_bot + NP * wb, wb, rowp(e->u[c], e->rows), pb, wb, 2 * NP,
+                         cudaMemcpyDeviceToDevice, e->stream));
+  }
+  const ncclDataType_t dt = e->elem == 8 ? ncclFloat64 : ncclFloat32;
+  NK(N.GroupStart());
+  if (has_prev) {
+    NK(N.Send(send_top, NP * w, dt, e->rank - 1, e->comm, e->stream));
+    NK(N.Recv(recv_top, 3 * NP * w, dt, e->rank - 1, e->comm, e->stream));
+  }
+  if (has_next) {
+    NK(N.Send(send_bot, 3 * NP * w, dt, e->rank + 1, e->comm, e->stream));
+    NK(N.Recv(recv_bot, NP * w, dt, e->rank + 1, e->comm, e->stream));
+  }
+  NK(N.GroupEnd());
+  if (has_prev) {
+    CK(cudaMemcpy2DAsync(rowp(e->phi[c], 0), pb, recv_top, wb, wb, NP, cudaMemcpyDeviceToDevice, e->stream));
+    CK(cudaMemcpy2DAsync(rowp(e->u[c], 0), pb, recv_top + NP * wb, wb, wb, 2 * NP,
+                         cudaMemcpyDeviceToDevice, e->stream));
+  }
+  if (has_next)
+    CK(cudaMemcpy2DAsync(rowp(e->phi[c], e->rows + 1), pb, recv_bot, wb, wb, NP,
+                         cudaMemcpyDeviceToDevice, e->stream));
+}
+
+static void enqueue_plain(otfx_engine* e, int64_t count) {
+  for (int64_t q = 0; q < count; ++q) {
+    launch_sweep(e, false);
+    exchange_nccl(e);
+  }
+}
+
+static void run_plain(otfx_engine* e, int64_t count) {
+  if (count <= 0) return;
+  if (!e->use_graphs || count < 3) {
+    enqueue_plain(e, count);
+    return;
+  }
+  auto key = std::make_pair(e->cur, count);
+  auto it = e->graphs.find(key);
+  if (it == e->graphs.end()) {
+    const int saved = e->cur;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_plain(e, count);
+    } catch (...) {
+      cudaStreamEndCapture(e->stream, &g);
+      e->cur = saved;
+      throw;
+    }
+    CK(cudaStreamEndCapture(e->stream, &g));
+    e->cur = saved;
+    cudaGraphExec_t ge;
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    it = e->graphs.emplace(key, ge).first;
+  }
+  CK(cudaGraphLaunch(it->second, e->stream));
+  e->cur ^= int(count & 1);
+}
+
+// raw scalars of the current iterate into d_raw (and h_raw after sync)
+static void raw_to_host(otfx_engine* e, bool with_res, bool allreduce) {
+  launch_evaluate(e);
+  reduce_raw_kernel<<<1, 256, 0, e->stream>>>(e->d_part_eval, e->d_max_eval, e->ex * e->ey,
+                                               e->d_part_sweep, e->gx * e->gy, with_res ? 1 : 0,
+                                               e->d_raw);
+  CK(cudaGetLastError());
+  if (allreduce && e->comm && e->nranks > 1) {
+    NcclApi& N = nccl();
+    NK(N.GroupStart());
+    NK(N.AllReduce(e->d_raw, e->d_raw, OTFX_NRAW_SUM, ncclFloat64, ncclSum, e->comm, e->stream));
+    NK(N.AllReduce(e->d_raw + OTFX_NRAW_SUM, e->d_raw + OTFX_NRAW_SUM, OTFX_NRAW - OTFX_NRAW_SUM,
+                   ncclFloat64, ncclMax, e->comm, e->stream));
+    NK(N.GroupEnd());
+  }
+  CK(cudaMemcpyAsync(e->h_raw, e->d_raw, OTFX_NRAW * sizeof(double), cudaMemcpyDeviceToHost,
+                     e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+}
+
+// S/solver.py:242-291 scalar algebra, same operation order
+static void finalize(const otfx_engine* e, const double* raw, double out[5]) {
+  const bool has_w = e->has_w;
+  const double alpha = e->d.alpha, eps = e->d.eps_reg;
+  double p = raw[R_PU];
+  if (has_w) p += alpha * raw[R_PW];
+  if (eps > 0) {
+    p += eps * raw[R_SU2];
+    if (has_w) p += eps * raw[R_SW2];
+  }
+  const double rawd = -raw[R_SPHID];
+  double dual;
+  if (eps == 0) {
+    double s = std::max(1.0, raw[R_GU]);
+    if (has_w) s = std::max(s, raw[R_GW] / alpha);
+    dual = rawd / s;
+  } else {
+    double pen = raw[R_PENU] / (4.0 * eps);
+    if (has_w) pen += raw[R_PENW] / (4.0 * eps);
+    dual = rawd - pen;
+  }
+  const double gap = (p - dual) / std::max(p, 1e-30);
+  const double tiny = 2.2250738585072014e-308;
+  const double feas = std::sqrt(raw[R_SCON]) / std::max(e->diff_norm, tiny);
+  double r = raw[R_SDU] / e->d.mu + raw[R_SDPHI] / e->d.tau;
+  if (has_w) r += raw[R_SDW] / e->d.nu;
+  r = r - 2.0 * raw[R_SCROSS];
+  out[0] = p;
+  out[1] = dual;
+  out[2] = gap;
+  out[3] = feas;
+  out[4] = r;
+}
+
+// ---- maps -----------------------------------------------------------------
+static void add_mass(PackMap& m, int idx) {
+  require(m.nmass < 16, OTFX_EUNSUPPORTED, "mass map overflow");
+  m.mass[m.nmass++] = idx;
+}
+
+// record layout of a potential-type payload (phi, diff, one u direction)
+// complex_rec: record holds complex128 entries
+static PackMap potential_pack(const otfx_engine* e, bool complex_rec) {
+  PackMap m;
+  memset(&m, 0, sizeof(m));
+  const int K = e->K;
+  m.np = e->NP;
+  switch (e->d.kind) {
+    case OTFX_KIND_SCALAR:
+      m.rec = 1;
+      m.src[0] = 0;
+      m.wt[0] = 1.0;
+      add_mass(m, 0);
+      break;
+    case OTFX_KIND_VECTOR:
+      m.rec = K;
+      for (int c = 0; c < K; ++c) {
+        m.src[c] = c;
+        m.wt[c] = 1.0;
+      }
+      break;
+    case OTFX_KIND_MATRIX_REAL: {
+      const int cs = complex_rec ? 2 : 1;
+      m.rec = cs * K * K;
+      for (int a = 0; a < K; ++a) {
+        m.src[a] = cs * (a * K + a);
+        m.wt[a] = 1.0;
+      }
+      for (int a = 0; a < K; ++a)
+        for (int b = a + 1; b < K; ++b) {
+          const int p = K + pair_index_rt(K, a, b);
+          m.src[p] = cs * (a * K + b);
+          m.wt[p] = 2.0;
+        }
+      break;
+    }
+    default: {
+      m.rec = 2 * K * K;
+      for (int a = 0; a < K; ++a) {
+        m.src[a] = 2 * (a * K + a);
+        m.wt[a] = 1.0;
+      }
+      for (int a = 0; a < K; ++a)
+        for (int b = a + 1; b < K; ++b) {
+          const int p = K + 2 * pair_index_rt(K, a, b);
+          m.src[p] = 2 * (a * K + b);
+          m.src[p + 1] = 2 * (a * K + b) + 1;
+          m.wt[p] = m.wt[p + 1] = 2.0;
+        }
+    }
+  }
+  return m;
+}
+
+}  // namespace otfx
+
+namespace otfx {
+
+static UnpackMap potential_unpack(const otfx_engine* e) {
+  UnpackMap m;
+  memset(&m, 0, sizeof(m));
+  const int K = e->K;
+  for (int q = 0; q < MAXMAP; ++q) {
+    m.plane[q] = -1;
+    m.sign[q] = 1;
+  }
+  switch (e->d.kind) {
+    case OTFX_KIND_SCALAR:
+      m.rec = 1;
+      m.plane[0] = 0;
+      break;
+    case OTFX_KIND_VECTOR:
+      m.rec = K;
+      for (int c = 0; c < K; ++c) m.plane[c] = c;
+      break;
+    case OTFX_KIND_MATRIX_REAL:
+      m.rec = K * K;
+      for (int a = 0; a < K; ++a)
+        for (int b = 0; b < K; ++b)
+          m.plane[a * K + b] = a == b ? a : K + pair_index_rt(K, std::min(a, b), std::max(a, b));
+      break;
+    default:
+      m.rec = 2 * K * K;
+      for (int a = 0; a < K; ++a)
+        for (int b = 0; b < K; ++b) {
+          const int q = 2 * (a * K + b);
+          if (a == b) {
+            m.plane[q] = a;
+          } else {
+            const int p = K + 2 * pair_index_rt(K, std::min(a, b), std::max(a, b));
+            m.plane[q] = p;
+            m.plane[q + 1] = p + 1;
+            m.sign[q + 1] = a < b ? 1 : -1;
+          }
+        }
+  }
+  return m;
+}
+
+static PackMap flux_w_pack(const otfx_engine* e) {
+  PackMap m;
+  memset(&m, 0, sizeof(m));
+  const int K = e->K, ell = e->d.ell;
+  m.np = e->NWact;
+  if (e->d.kind == OTFX_KIND_VECTOR) {
+    m.rec = ell;
+    for (int q = 0; q < ell; ++q) {
+      m.src[q] = q;
+      m.wt[q] = 1.0;
+    }
+    return m;
+  }
+  m.rec = 2 * ell * K * K;
+  const int NWS = e->NWS;
+  for (int s = 0; s < ell; ++s) {
+    const int base = 2 * s * K * K;
+    if (e->d.kind == OTFX_KIND_MATRIX_REAL) {
+      for (int a = 0; a < K; ++a)
+        for (int b = a + 1; b < K; ++b) {
+          const int p = s * NWS + pair_index_rt(K, a, b);
+          m.src[p] = base + 2 * (a * K + b);
+          m.wt[p] = 2.0;
+        }
+    } else {
+      for (int a = 0; a < K; ++a) {
+        m.src[s * NWS + a] = base + 2 * (a * K + a) + 1;
+        m.wt[s * NWS + a] = 1.0;
+      }
+      for (int a = 0; a < K; ++a)
+        for (int b = a + 1; b < K; ++b) {
+          const int p = s * NWS + K + 2 * pair_index_rt(K, a, b);
+          m.src[p] = base + 2 * (a * K + b);
+          m.src[p + 1] = base + 2 * (a * K + b) + 1;
+          m.wt[p] = m.wt[p + 1] = 2.0;
+        }
+    }
+  }
+  return m;
+}
+
+static UnpackMap flux_w_unpack(const otfx_engine* e) {
+  UnpackMap m;
+  memset(&m, 0, sizeof(m));
+  for (int q = 0; q < MAXMAP; ++q) {
+    m.plane[q] = -1;
+    m.sign[q] = 1;
+  }
+  const int K = e->K, ell = e->d.ell;
+  if (e->d.kind == OTFX_KIND_VECTOR) {
+    m.rec = ell;
+    for (int q = 0; q < ell; ++q) m.plane[q] = q;
+    return m;
+  }
+  m.rec = 2 * ell * K * K;
+  const int NWS = e->NWS;
+  for (int s = 0; s < ell; ++s) {
+    const int base = 2 * s * K * K;
+    for (int a = 0; a < K; ++a)
+      for (int b = 0; b < K; ++b) {
+        const int q = base + 2 * (a * K + b);
+        if (e->d.kind == OTFX_KIND_MATRIX_REAL) {
+          if (a == b) continue;
+          m.plane[q] = s * NWS + pair_index_rt(K, std::min(a, b), std::max(a, b));
+          m.sign[q] = a < b ? 1 : -1;
+        } else if (a == b) {
+          m.plane[q + 1] = s * NWS + a;
+        } else {
+          const int p = s * NWS + K + 2 * pair_index_rt(K, std::min(a, b), std::max(a, b));
+          m.plane[q] = p;
+          m.sign[q] = a < b ? 1 : -1;
+          m.plane[q + 1] = p + 1;
+        }
+      }
+  }
+  return m;
+}
+
+// ---- host <-> device transfers -------------------------------------------
+template <typename T>
+static void pack_chunk(otfx_engine* e, const double* s0, const double* s1, int64_t ncell,
+                       void* planes, int lrow0, const PackMap& m) {
+  pack_kernel<T><<<kPackBlocks, 256, 0, e->stream>>>(s0, s1, ncell, e->d.n, static_cast<T*>(planes),
+                                                     e->plane, e->pitch, lrow0, m, e->d_pack_part);
+  CK(cudaGetLastError());
+}
+
+// upload rows of host records (reference layout) into planes; returns the
+// summed block partials {mass0, mass1, weighted sumsq}
+static void host_to_planes(otfx_engine* e, const double* h0, const double* h1, const PackMap& m,
+                           void* planes, double sums[3]) {
+  const int n = e->d.n;
+  const size_t row_bytes = size_t(n) * m.rec * sizeof(double);
+  const int inputs = h1 ? 2 : 1;
+  int chunk = int(std::max<size_t>(1, e->stage_bytes / (inputs * row_bytes)));
+  chunk = std::min(chunk, e->rows);
+  require(size_t(chunk) * row_bytes * inputs <= e->stage_bytes, OTFX_EUNSUPPORTED,
+          "grid row too large for the staging buffer");
+  sums[0] = sums[1] = sums[2] = 0.0;
+  double* st0 = e->d_stage;
+  double* st1 = e->d_stage + size_t(chunk) * n * m.rec;
+  for (int r0 = 0; r0 < e->rows; r0 += chunk) {
+    const int nr = std::min(chunk, e->rows - r0);
+    const size_t off = size_t(r0) * n * m.rec;
+    const size_t bytes = size_t(nr) * row_bytes;
+    CK(cudaMemcpyAsync(st0, h0 + off, bytes, cudaMemcpyHostToDevice, e->stream));
+    if (h1) CK(cudaMemcpyAsync(st1, h1 + off, bytes, cudaMemcpyHostToDevice, e->stream));
+    if (e->elem == 8) pack_chunk<double>(e, st0, h1 ? st1 : nullptr, int64_t(nr) * n, planes, 1 + r0, m);
+    else pack_chunk<float>(e, st0, h1 ? st1 : nullptr, int64_t(nr) * n, planes, 1 + r0, m);
+    CK(cudaMemcpyAsync(e->h_pack_part, e->d_pack_part, kPackBlocks * 3 * sizeof(double),
+                       cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    for (int b = 0; b < kPackBlocks; ++b)
+      for (int q = 0; q < 3; ++q) sums[q] += e->h_pack_part[b * 3 + q];
+  }
+}
+
+static void planes_to_host(otfx_engine* e, const void* planes, const UnpackMap& m, double* h) {
+  const int n = e->d.n;
+  const size_t row_bytes = size_t(n) * m.rec * sizeof(double);
+  int chunk = int(std::max<size_t>(1, e->stage_bytes / row_bytes));
+  chunk = std::min(chunk, e->rows);
+  for (int r0 = 0; r0 < e->rows; r0 += chunk) {
+    const int nr = std::min(chunk, e->rows - r0);
+    const int64_t ncell = int64_t(nr) * n;
+    if (e->elem == 8)
+      unpack_kernel<double><<<kPackBlocks, 256, 0, e->stream>>>(
+          static_cast<const double*>(planes), e->plane, e->pitch, 1 + r0, ncell, n, m, e->d_stage);
+    else
+      unpack_kernel<float><<<kPackBlocks, 256, 0, e->stream>>>(
+          static_cast<const float*>(planes), e->plane, e->pitch, 1 + r0, ncell, n, m, e->d_stage);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h + size_t(r0) * n * m.rec, e->d_stage, size_t(nr) * row_bytes,
+                       cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+  }
+}
+
+static void* plane_ptr(otfx_engine* e, void* base, int p) {
+  return static_cast<char*>(base) + size_t(p) * e->plane * e->elem;
+}
+
+static void allreduce_host(otfx_engine* e, double* v, int count) {
+  if (!e->comm || e->nranks == 1) return;
+  CK(cudaMemcpyAsync(e->d_raw, v, count * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  NK(nccl().AllReduce(e->d_raw, e->d_raw, count, ncclFloat64, ncclSum, e->comm, e->stream));
+  CK(cudaMemcpyAsync(v, e->d_raw, count * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+}
+
+static void drop_graphs(otfx_engine* e) {
+  for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
+  e->graphs.clear();
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+static void create(const otfx_engine_desc* d, otfx_engine* e) {
+  require(d != nullptr, OTFX_EINVAL, "null descriptor");
+  e->d = *d;
+  const int kind = d->kind;
+  require(kind >= 0 && kind <= 3, OTFX_EINVAL, "unknown kind");
+  require(d->dtype == OTFX_F64 || d->dtype == OTFX_F32, OTFX_EINVAL, "unknown dtype");
+  require(d->n >= 2, OTFX_EINVAL, "grid needs n >= 2");
+  require(d->row_begin >= 0 && d->row_end <= d->n && d->row_begin < d->row_end, OTFX_EINVAL,
+          "bad slab rows");
+  require(d->tau > 0 && d->mu > 0, OTFX_EINVAL, "step sizes must be positive");
+  require(d->norm_u >= 0 && d->norm_u <= 3 && d->norm_w >= 0 && d->norm_w <= 3, OTFX_EINVAL,
+          "unknown norm family");
+  e->elem = d->dtype == OTFX_F64 ? 8 : 4;
+  e->K = kind == OTFX_KIND_SCALAR ? 1 : d->k;
+  if (d->dtype == OTFX_F64) e->ops64 = find_ops<double>(kind, e->K);
+  else e->ops32 = find_ops<float>(kind, e->K);
+  const bool found = e->ops64 || e->ops32;
+  require(found, OTFX_EUNSUPPORTED,
+          "no sm_100a instantiation for kind=" + std::to_string(kind) + " k=" + std::to_string(e->K));
+  const int NP = e->ops64 ? e->ops64->NP : e->ops32->NP;
+  const int NWS = e->ops64 ? e->ops64->NWS : e->ops32->NWS;
+  const int LMAX = e->ops64 ? e->ops64->LMAX : e->ops32->LMAX;
+  e->has_w = e->ops64 ? e->ops64->has_w : e->ops32->has_w;
+  e->NP = NP;
+  e->NWS = NWS;
+  e->LMAX = LMAX;
+  if (e->has_w) {
+    require(d->ell >= 1 && d->ell <= LMAX, OTFX_EUNSUPPORTED,
+            "channel count ell=" + std::to_string(d->ell) + " exceeds the instantiation capacity " +
+                std::to_string(LMAX));
+    require(d->nu > 0 && d->alpha > 0, OTFX_EINVAL, "nu and alpha must be positive");
+    require(d->chan != nullptr, OTFX_EINVAL, "channel operator missing");
+    const size_t nc = kind == OTFX_KIND_VECTOR ? size_t(e->K) * d->ell : size_t(d->ell) * e->K * e->K * 2;
+    require(nc <= size_t(MAX_CHAN_COEF), OTFX_EUNSUPPORTED, "channel operator too large");
+    e->chan.assign(d->chan, d->chan + nc);
+    e->NWact = d->ell * NWS;
+  } else {
+    e->d.ell = 0;
+    e->NWact = 0;
+  }
+  if (kind == OTFX_KIND_VECTOR || kind == OTFX_KIND_SCALAR)
+    require(d->norm_u != OTFX_NORM_L1NUC && d->norm_w != OTFX_NORM_L1NUC, OTFX_EUNSUPPORTED,
+            "nuclear norm requires a matrix payload");
+  if (kind == OTFX_KIND_MATRIX_REAL)
+    require(d->norm_u != OTFX_NORM_L1NUC && d->norm_w != OTFX_NORM_L1NUC, OTFX_EINVAL,
+            "nuclear norms run on the complex path");
+  require(!(e->has_w && d->norm_w == OTFX_NORM_L12), OTFX_EUNSUPPORTED,
+          "row-grouped norm applies only to spatial fluxes");
+  require(!(d->eps_reg > 0 && (d->norm_u == OTFX_NORM_L1NUC || d->norm_w == OTFX_NORM_L1NUC)),
+          OTFX_EUNSUPPORTED, "eps_reg > 0 has no closed-form prox for the nuclear family");
+
+  CK(cudaSetDevice(d->device));
+  if (d->stream) {
+    e->stream = static_cast<cudaStream_t>(d->stream);
+  } else {
+    CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    e->own_stream = true;
+  }
+  e->rows = d->row_end - d->row_begin;
+  e->rows_alloc = e->rows + 2;
+  e->pitch = (d->n + 31) / 32 * 32;
+  e->plane = int64_t(e->rows_alloc) * e->pitch;
+  const int per_state = 3 * NP + e->NWact;
+  const size_t pb = size_t(e->plane) * e->elem;
+  e->state_bytes = size_t(per_state) * pb;
+
+  // sweep geometry: TX columns per CTA, R rows per CTA, >= ~4 CTAs per SM
+  const int n = d->n;
+  e->TX = env_int("OTFX_TILE_COLS", n > 64 ? 128 : (n > 32 ? 64 : 32));
+  e->gx = (n + e->TX - 1) / e->TX;
+  const int want = 148 * 4;
+  int gy = (want + e->gx - 1) / e->gx;
+  int R = (e->rows + gy - 1) / gy;
+  R = std::max(4, std::min(64, R));
+  R = env_int("OTFX_TILE_ROWS", R);
+  e->R = R;
+  e->gy = (e->rows + R - 1) / R;
+  const size_t sw = size_t(e->TX + 1) * NP * 2 * e->elem;
+  e->smem_plain = ((2 * sw + 15) & ~size_t(15)) + 32 * 4 * sizeof(double);
+  e->smem_check = ((3 * sw + 15) & ~size_t(15)) + 32 * 4 * sizeof(double);
+  e->ex = (n + 127) / 128;
+  e->ey = e->rows;
+
+  // staging: up to 64 MB, at least two grid rows of the widest record
+  const int max_rec = std::max(2 * e->K * e->K * std::max(1, d->ell) * 2, 16);
+  e->stage_bytes = std::max<size_t>(size_t(64) << 20, size_t(2) * n * max_rec * sizeof(double));
+
+  const size_t n_sweep = size_t(e->gx) * e->gy * 4, n_pe = size_t(e->ex) * e->ey * 8,
+               n_me = size_t(e->ex) * e->ey * 2;
+  const size_t halo = size_t(8) * NP * n * e->elem;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_state0 = carve(e->state_bytes), o_state1 = carve(e->state_bytes);
+  const size_t o_diff = carve(size_t(NP) * pb);
+  const size_t o_ps = carve(n_sweep * 8), o_pe = carve(n_pe * 8), o_me = carve(n_me * 8);
+  const size_t o_raw = carve(64 * 8);
+  const size_t o_pack = carve(kPackBlocks * 3 * 8);
+  const size_t o_halo = carve(halo);
+  const size_t o_stage = carve(e->stage_bytes);
+  e->total_bytes = off;
+  CK(cudaMalloc(&e->mem, off));
+  CK(cudaMemsetAsync(e->mem, 0, o_stage, e->stream));
+  for (int s = 0; s < 2; ++s) {
+    unsigned char* b = e->mem + (s ? o_state1 : o_state0);
+    e->u[s] = b;
+    e->phi[s] = b + size_t(2 * NP) * pb;
+    e->w[s] = b + size_t(3 * NP) * pb;
+  }
+  e->diff = e->mem + o_diff;
+  e->d_part_sweep = reinterpret_cast<double*>(e->mem + o_ps);
+  e->d_part_eval = reinterpret_cast<double*>(e->mem + o_pe);
+  e->d_max_eval = reinterpret_cast<double*>(e->mem + o_me);
+  e->d_raw = reinterpret_cast<double*>(e->mem + o_raw);
+  e->d_pack_part = reinterpret_cast<double*>(e->mem + o_pack);
+  e->d_halo = e->mem + o_halo;
+  e->d_stage = reinterpret_cast<double*>(e->mem + o_stage);
+  CK(cudaMallocHost(&e->h_raw, 64 * sizeof(double)));
+  CK(cudaMallocHost(&e->h_pack_part, kPackBlocks * 3 * sizeof(double)));
+  CK(e->ops64 ? e->ops64->prepare() : e->ops32->prepare());
+  e->use_graphs = env_int("OTFX_GRAPHS", 1) != 0;
+  CK(cudaStreamSynchronize(e->stream));
+}
+
+static void destroy(otfx_engine* e) {
+  if (!e) return;
+  drop_graphs(e);
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  if (e->comm && nccl().CommDestroy) nccl().CommDestroy(e->comm);
+  if (e->mem) cudaFree(e->mem);
+  if (e->h_raw) cudaFreeHost(e->h_raw);
+  if (e->h_pack_part) cudaFreeHost(e->h_pack_part);
+  if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
+}
+
+static void zero_state(otfx_engine* e) {
+  for (int s = 0; s < 2; ++s) {
+    CK(cudaMemsetAsync(e->u[s], 0, e->state_bytes, e->stream));
+  }
+  e->cur = 0;
+  e->residual_valid = false;
+  CK(cudaStreamSynchronize(e->stream));
+}
+
+}  // namespace otfx
+
+// ===========================================================================
+// extern "C" ABI
+// ===========================================================================
+using namespace otfx;
+
+#define API_BEGIN try {
+#define API_END                        \
+  }                                    \
+  catch (const Error& ex) {            \
+    g_err = ex.what();                 \
+    return ex.code;                    \
+  }                                    \
+  catch (const std::exception& ex) {   \
+    g_err = ex.what();                 \
+    return OTFX_ECUDA;                 \
+  }                                    \
+  return OTFX_OK;
+
+extern "C" {
+
+int otfx_abi_version(void) { return OTFX_ABI_VERSION; }
+
+const char* otfx_last_error(void) { return g_err.c_str(); }
+
+int otfx_device_count(int* count) {
+  API_BEGIN
+  require(count != nullptr, OTFX_EINVAL, "null pointer");
+  int c = 0;
+  cudaError_t err = cudaGetDeviceCount(&c);
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *count = c;
+  API_END
+}
+
+int otfx_engine_create(const otfx_engine_desc* desc, otfx_engine** out) {
+  API_BEGIN
+  require(out != nullptr, OTFX_EINVAL, "null output pointer");
+  *out = nullptr;
+  std::unique_ptr<otfx_engine> e(new otfx_engine());
+  try {
+    create(desc, e.get());
+  } catch (...) {
+    destroy(e.get());
+    throw;
+  }
+  *out = e.release();
+  API_END
+}
+
+int otfx_engine_destroy(otfx_engine* e) {
+  API_BEGIN
+  if (e) {
+    destroy(e);
+    delete e;
+  }
+  API_END
+}
+
+int otfx_engine_get_info(otfx_engine* e, otfx_engine_info* info) {
+  API_BEGIN
+  require(e && info, OTFX_EINVAL, "null pointer");
+  info->state_bytes = int64_t(e->state_bytes);
+  info->total_bytes = int64_t(e->total_bytes);
+  info->np = e->NP;
+  info->nws = e->NWS;
+  info->lmax = e->LMAX;
+  info->pitch = e->pitch;
+  info->tile_cols = e->TX;
+  info->tile_rows = e->R;
+  info->grid_x = e->gx;
+  info->grid_y = e->gy;
+  info->regs_plain = e->ops64 ? e->ops64->sweep_regs(false) : e->ops32->sweep_regs(false);
+  info->regs_check = e->ops64 ? e->ops64->sweep_regs(true) : e->ops32->sweep_regs(true);
+  info->graphs = e->use_graphs ? 1 : 0;
+  API_END
+}
+
+int otfx_engine_set_marginals(otfx_engine* e, const double* l0, const double* l1, double masses[2]) {
+  API_BEGIN
+  require(e && l0 && l1, OTFX_EINVAL, "null pointer");
+  CK(cudaSetDevice(e->d.device));
+  PackMap m = potential_pack(e, e->d.kind >= OTFX_KIND_MATRIX_REAL);
+  if (e->d.kind == OTFX_KIND_VECTOR) {
+    for (int c = 0; c < e->K; ++c) add_mass(m, c);
+  } else if (e->d.kind >= OTFX_KIND_MATRIX_REAL) {
+    for (int a = 0; a < e->K; ++a) add_mass(m, 2 * (a * e->K + a));
+  }
+  double sums[3];
+  host_to_planes(e, l0, l1, m, e->diff, sums);
+  allreduce_host(e, sums, 3);
+  e->diff_norm = std::sqrt(sums[2]);
+  if (masses) {
+    masses[0] = sums[0];
+    masses[1] = sums[1];
+  }
+  API_END
+}
+
+int otfx_engine_set_diff(otfx_engine* e, const double* diff) {
+  API_BEGIN
+  require(e && diff, OTFX_EINVAL, "null pointer");
+  CK(cudaSetDevice(e->d.device));
+  PackMap m = potential_pack(e, e->d.kind == OTFX_KIND_MATRIX_COMPLEX);
+  double sums[3];
+  host_to_planes(e, diff, nullptr, m, e->diff, sums);
+  allreduce_host(e, sums, 3);
+  e->diff_norm = std::sqrt(sums[2]);
+  API_END
+}
+
+int otfx_engine_diff_norm(otfx_engine* e, double* get, const double* set) {
+  API_BEGIN
+  require(e, OTFX_EINVAL, "null engine");
+  if (get) *get = e->diff_norm;
+  if (set) e->diff_norm = *set;
+  API_END
+}
+
+int otfx_engine_zero_state(otfx_engine* e) {
+  API_BEGIN
+  require(e, OTFX_EINVAL, "null engine");
+  CK(cudaSetDevice(e->d.device));
+  zero_state(e);
+  API_END
+}
+
+int otfx_engine_set_state(otfx_engine* e, const double* ux, const double* uy, const double* w,
+                          const double* phi) {
+  API_BEGIN
+  require(e && ux && uy && phi, OTFX_EINVAL, "null pointer");
+  require(!e->has_w || w, OTFX_EINVAL, "channel flux missing");
+  CK(cudaSetDevice(e->d.device));
+  zero_state(e);
+  const int c = e->cur;
+  PackMap pm = potential_pack(e, e->d.kind == OTFX_KIND_MATRIX_COMPLEX);
+  double sums[3];
+  host_to_planes(e, ux, nullptr, pm, e->u[c], sums);
+  host_to_planes(e, uy, nullptr, pm, plane_ptr(e, e->u[c], e->NP), sums);
+  host_to_planes(e, phi, nullptr, pm, e->phi[c], sums);
+  if (e->has_w) host_to_planes(e, w, nullptr, flux_w_pack(e), e->w[c], sums);
+  exchange_nccl(e);
+  CK(cudaStreamSynchronize(e->stream));
+  API_END
+}
+
+int otfx_engine_get_state(otfx_engine* e, double* ux, double* uy, double* w, double* phi) {
+  API_BEGIN
+  require(e, OTFX_EINVAL, "null engine");
+  CK(cudaSetDevice(e->d.device));
+  const int c = e->cur;
+  UnpackMap pm = potential_unpack(e);
+  if (ux) planes_to_host(e, e->u[c], pm, ux);
+  if (uy) planes_to_host(e, plane_ptr(e, e->u[c], e->NP), pm, uy);
+  if (phi) planes_to_host(e, e->phi[c], pm, phi);
+  if (w && e->has_w) planes_to_host(e, e->w[c], flux_w_unpack(e), w);
+  API_END
+}
+
+int otfx_engine_step(otfx_engine* e, int64_t iters) {
+  API_BEGIN
+  require(e, OTFX_EINVAL, "null engine");
+  require(iters >= 0, OTFX_EINVAL, "negative iteration count");
+  CK(cudaSetDevice(e->d.device));
+  run_plain(e, iters);
+  e->residual_valid = false;
+  API_END
+}
+
+int otfx_engine_sweep(otfx_engine* e, int check) {
+  API_BEGIN
+  require(e, OTFX_EINVAL, "null engine");
+  CK(cudaSetDevice(e->d.device));
+  launch_sweep(e, check != 0);
+  e->residual_valid = check != 0;
+  API_END
+}
+
+int otfx_engine_evaluate(otfx_engine* e, double out[4]) {
+  API_BEGIN
+  require(e && out, OTFX_EINVAL, "null pointer");
+  CK(cudaSetDevice(e->d.device));
+  raw_to_host(e, false, true);
+  double r[5];
+  finalize(e, e->h_raw, r);
+  for (int q = 0; q < 4; ++q) out[q] = r[q];
+  API_END
+}
+
+int otfx_engine_step_check(otfx_engine* e, double out[5]) {
+  API_BEGIN
+  require(e && out, OTFX_EINVAL, "null pointer");
+  CK(cudaSetDevice(e->d.device));
+  launch_sweep(e, true);
+  exchange_nccl(e);
+  raw_to_host(e, true, true);
+  finalize(e, e->h_raw, out);
+  API_END
+}
+
+int otfx_engine_raw(otfx_engine* e, int with_residual, double raw[OTFX_NRAW]) {
+  API_BEGIN
+  require(e && raw, OTFX_EINVAL, "null pointer");
+  require(!with_residual || e->residual_valid, OTFX_EINVAL, "no check sweep since the last step");
+  CK(cudaSetDevice(e->d.device));
+  raw_to_host(e, with_residual != 0, false);
+  for (int q = 0; q < OTFX_NRAW; ++q) raw[q] = e->h_raw[q];
+  API_END
+}
+
+int otfx_engine_finalize(otfx_engine* e, const double raw[OTFX_NRAW], double out[5]) {
+  API_BEGIN
+  require(e && raw && out, OTFX_EINVAL, "null pointer");
+  finalize(e, raw, out);
+  API_END
+}
+
+int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_point* hist,
+                    int64_t capacity, int64_t* n_history, int64_t* iterations, int* converged,
+                    double* wall_seconds) {
+  API_BEGIN
+  require(e && cfg && hist && n_history && iterations && converged, OTFX_EINVAL, "null pointer");
+  require(cfg->max_iters >= 1 && cfg->check_every >= 1, OTFX_EINVAL,
+          "max_iters and check_every must be >= 1");
+  CK(cudaSetDevice(e->d.device));
+  const auto t0 = std::chrono::steady_clock::now();
+  int64_t nh = 0;
+  auto push = [&](int64_t it, const double* r, double rk) {
+    require(nh < capacity, OTFX_EINVAL, "history buffer too small");
+    hist[nh++] = {double(it), r[0], r[1], r[2], r[3], rk};
+  };
+  double r[5];
+  raw_to_host(e, false, true);
+  finalize(e, e->h_raw, r);
+  push(0, r, std::nan(""));
+  bool conv = r[2] <= cfg->tol_gap && r[3] <= cfg->tol_feas;
+  int64_t it = 0;
+  const int64_t ce = cfg->check_every, mx = cfg->max_iters;
+  while (!conv && it < mx) {
+    const int64_t next = std::min((it / ce + 1) * ce, mx);
+    run_plain(e, next - it - 1);
+    it = next - 1;
+    launch_sweep(e, true);
+    exchange_nccl(e);
+    raw_to_host(e, true, true);
+    finalize(e, e->h_raw, r);
+    ++it;
+    push(it, r, r[4]);
+    conv = r[2] <= cfg->tol_gap && r[3] <= cfg->tol_feas;
+  }
+  *n_history = nh;
+  *iterations = it;
+  *converged = conv ? 1 : 0;
+  if (wall_seconds)
+    *wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  API_END
+}
+
+int otfx_engine_residual_between(otfx_engine* e, const double* ux0, const double* uy0,
+                                 const double* w0, const double* phi0, const double* ux1,
+                                 const double* uy1, const double* w1, const double* phi1,
+                                 double* out) {
+  API_BEGIN
+  require(e && ux0 && uy0 && phi0 && ux1 && uy1 && phi1 && out, OTFX_EINVAL, "null pointer");
+  require(!e->has_w || (w0 && w1), OTFX_EINVAL, "channel flux missing");
+  require(e->rows == e->d.n, OTFX_EINVAL, "residual_between needs a whole-grid engine");
+  CK(cudaSetDevice(e->d.device));
+  zero_state(e);
+  PackMap pm = potential_pack(e, e->d.kind == OTFX_KIND_MATRIX_COMPLEX);
+  double sums[3];
+  const double* src[2][4] = {{ux0, uy0, w0, phi0}, {ux1, uy1, w1, phi1}};
+  for (int s = 0; s < 2; ++s) {
+    host_to_planes(e, src[s][0], nullptr, pm, e->u[s], sums);
+    host_to_planes(e, src[s][1], nullptr, pm, plane_ptr(e, e->u[s], e->NP), sums);
+    host_to_planes(e, src[s][3], nullptr, pm, e->phi[s], sums);
+    if (e->has_w) host_to_planes(e, src[s][2], nullptr, flux_w_pack(e), e->w[s], sums);
+  }
+  if (e->elem == 8) {
+    SweepArgs<double> a = make_args<double>(e, 0);
+    a.partials = e->d_part_eval;
+    a.maxes = e->d_max_eval;
+    CK(e->ops64->residual(a, dim3(e->ex, e->ey), dim3(128), e->stream));
+  } else {
+    SweepArgs<float> a = make_args<float>(e, 0);
+    a.partials = e->d_part_eval;
+    a.maxes = e->d_max_eval;
+    CK(e->ops32->residual(a, dim3(e->ex, e->ey), dim3(128), e->stream));
+  }
+  reduce_raw_kernel<<<1, 256, 0, e->stream>>>(e->d_part_eval, e->d_max_eval, e->ex * e->ey,
+                                               e->d_part_sweep, 0, 0, e->d_raw);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(e->h_raw, e->d_raw, OTFX_NRAW * sizeof(double), cudaMemcpyDeviceToHost,
+                     e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  const double* r = e->h_raw;
+  double v = r[0] / e->d.mu + r[2] / e->d.tau;
+  if (e->has_w) v += r[1] / e->d.nu;
+  *out = v - 2.0 * r[3];
+  zero_state(e);
+  API_END
+}
+
+int otfx_engine_exchange_local(otfx_engine* const* es, int count) {
+  API_BEGIN
+  require(es && count >= 1, OTFX_EINVAL, "no engines");
+  for (int s = 0; s + 1 < count; ++s) {
+    otfx_engine* a = es[s];
+    otfx_engine* b = es[s + 1];
+    require(a->stream == b->stream, OTFX_EINVAL, "local exchange needs one shared stream");
+    require(a->d.row_end == b->d.row_begin && a->d.n == b->d.n && a->elem == b->elem &&
+                a->NP == b->NP && a->pitch == b->pitch,
+            OTFX_EINVAL, "engines are not adjacent slabs of one grid");
+    require(a->cur == b->cur, OTFX_EINVAL, "engines are at different iterations");
+    const int c = a->cur;
+    CK(cudaSetDevice(a->d.device));
+    // a's bottom ghost <- b's first row (phi)
+    copy_rows(a, a->phi[c], a->rows + 1, b, b->phi[c], 1, a->NP, a->stream);
+    // b's top ghost <- a's last row (phi, u)
+    copy_rows(b, b->phi[c], 0, a, a->phi[c], a->rows, a->NP, a->stream);
+    copy_rows(b, b->u[c], 0, a, a->u[c], a->rows, 2 * a->NP, a->stream);
+  }
+  API_END
+}
+
+int otfx_nccl_unique_id(unsigned char id[128]) {
+  API_BEGIN
+  require(id, OTFX_EINVAL, "null pointer");
+  ncclUniqueId u;
+  NK(nccl().GetUniqueId(&u));
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  memcpy(id, &u, 128);
+  API_END
+}
+
+int otfx_engine_attach_nccl(otfx_engine* e, const unsigned char id[128], int nranks, int rank) {
+  API_BEGIN
+  require(e && id, OTFX_EINVAL, "null pointer");
+  require(nranks >= 1 && rank >= 0 && rank < nranks, OTFX_EINVAL, "bad rank");
+  CK(cudaSetDevice(e->d.device));
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  NK(nccl().CommInitRank(&e->comm, nranks, u, rank));
+  e->nranks = nranks;
+  e->rank = rank;
+  drop_graphs(e);
+  API_END
+}
+
+int otfx_engine_sync(otfx_engine* e) {
+  API_BEGIN
+  require(e, OTFX_EINVAL, "null engine");
+  CK(cudaStreamSynchronize(e->stream));
+  API_END
+}
+
+void* otfx_engine_stream(otfx_engine* e) { return e ? static_cast<void*>(e->stream) : nullptr; }
+
+}  // extern "C"

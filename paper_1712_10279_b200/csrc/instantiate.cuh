@@ -1,0 +1,47 @@
+// Builds an Ops<T> table entry for one payload policy.
+#pragma once
+
+#include "ops.h"
+#include "sweep.cuh"
+
+namespace otfx {
+
+template <class P, typename T>
+struct OpsFor {
+  static cudaError_t prepare() {
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<P, T, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(sweep_kernel<P, T, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  }
+  static cudaError_t sweep(const SweepArgs<T>& a, dim3 g, dim3 b, size_t smem, cudaStream_t s,
+                           bool check) {
+    if (check)
+      sweep_kernel<P, T, true><<<g, b, smem, s>>>(a);
+    else
+      sweep_kernel<P, T, false><<<g, b, smem, s>>>(a);
+    return cudaGetLastError();
+  }
+  static cudaError_t evaluate(const SweepArgs<T>& a, dim3 g, dim3 b, cudaStream_t s) {
+    evaluate_kernel<P, T><<<g, b, 0, s>>>(a);
+    return cudaGetLastError();
+  }
+  static cudaError_t residual(const SweepArgs<T>& a, dim3 g, dim3 b, cudaStream_t s) {
+    residual_kernel<P, T><<<g, b, 0, s>>>(a);
+    return cudaGetLastError();
+  }
+  static int regs(bool check) {
+    cudaFuncAttributes at;
+    if (check) cudaFuncGetAttributes(&at, sweep_kernel<P, T, true>);
+    else cudaFuncGetAttributes(&at, sweep_kernel<P, T, false>);
+    return at.numRegs;
+  }
+  static const Ops<T>* table(int kind) {
+    static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
+                             P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &regs};
+    return &o;
+  }
+};
+
+}  // namespace otfx

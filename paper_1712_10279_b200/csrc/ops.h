@@ -1,0 +1,35 @@
+// Host-side dispatch table: one Ops<T> per (payload policy, precision).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace otfx {
+
+template <typename T>
+struct Ops {
+  int kind;
+  int K;      // channels / matrix dimension
+  int NP;     // reals per potential (and per flux direction)
+  int NWS;    // reals per channel block (edge / Lindblad matrix)
+  int LMAX;   // channel-block capacity of the instantiation
+  bool has_w;
+  cudaError_t (*prepare)();  // raise dynamic smem limits once
+  cudaError_t (*sweep)(const SweepArgs<T>& a, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       bool check);
+  cudaError_t (*evaluate)(const SweepArgs<T>& a, dim3 grid, dim3 block, cudaStream_t s);
+  cudaError_t (*residual)(const SweepArgs<T>& a, dim3 grid, dim3 block, cudaStream_t s);
+  int (*sweep_regs)(bool check);
+};
+
+// registries, one per instantiation unit
+const Ops<double>* ops_vector_f64(int K, bool has_w);
+const Ops<float>* ops_vector_f32(int K, bool has_w);
+const Ops<double>* ops_matrix_f64(int kind, int K);
+const Ops<float>* ops_matrix_f32(int kind, int K);
+
+template <typename T>
+const Ops<T>* find_ops(int kind, int K);
+
+}  // namespace otfx

@@ -97,3 +97,28 @@ def dirac_pair(n, cell0, cell1):
     a[cell0] = 1.0
     b[cell1] = 1.0
     return a, b
+
+
+def rgb_disk_rows(n, r0, r1, radius=DISK_RADIUS, chunk=2048):
+    """Rows [r0, r1) of rgb_disk_pair(n) without materialising the whole grid
+    (for row-slab runs at 8192^2 and beyond).  Masks use the same
+    floating-point predicate; the normaliser is accumulated chunk-wise, so the
+    result can differ from rgb_disk_pair(n)[r0:r1] in the last bit."""
+    x = _centres(n)
+    counts = []
+    for centre in DISK_CENTERS:
+        c = 0
+        for a in range(0, n, chunk):
+            c += int(np.count_nonzero(
+                (x[a:a + chunk, None] - centre[0]) ** 2 + (x[None, :] - centre[1]) ** 2
+                <= radius ** 2))
+        counts.append(c)
+    total = float(sum(c * (1.0 / c) for c in counts))
+    out = []
+    for shift in (0, 1):
+        v = np.zeros((r1 - r0, n, 3))
+        for ch, centre in enumerate(DISK_CENTERS):
+            m = (x[r0:r1, None] - centre[0]) ** 2 + (x[None, :] - centre[1]) ** 2 <= radius ** 2
+            v[m, (ch + shift) % 3] += 1.0 / counts[ch]
+        out.append(v / total)
+    return out[0], out[1]

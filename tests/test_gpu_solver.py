@@ -1,0 +1,268 @@
+"""GPU behaviour tests mirroring the reference suite (T/test_solver.py) plus
+oracle parity on seeded random inputs, determinism, slab decomposition and the
+standalone metric helpers."""
+
+import numpy as np
+import pytest
+
+import gpu_util as g
+import paper_1712_10279_b200 as pk
+from oracle import pdhg
+from paper_1712_10279_b200 import synthetic
+from paper_1712_10279_b200.solver import CudaEngine, build_engine, exchange_local
+
+pytestmark = pytest.mark.gpu
+
+
+def _norm_rand(rng, shape):
+    v = rng.random(shape)
+    return v / v.sum()
+
+
+def _rand_herm_psd(rng, n, k):
+    a = rng.normal(size=(n, n, k, k)) + 1j * rng.normal(size=(n, n, k, k))
+    p = a @ np.conj(np.swapaxes(a, -1, -2))
+    tr = np.sum(np.real(np.trace(p, axis1=2, axis2=3)))
+    return pk.MatrixDensity(p / tr)
+
+
+def _oracle_vector(l0, l1, graph, cfg, iters, check_every):
+    n = l0.shape[0]
+    tau = cfg.tau if cfg.tau is not None else pk.default_tau(n)
+    eng = pdhg.OracleEngine("vector", l0 - l1, n, tau, norm_u=cfg.norm_u.value,
+                            norm_w=cfg.norm_w.value, alpha=cfg.alpha, eps=cfg.eps_reg,
+                            chan=graph.coefficients(), lam_chan=pk.lambda_max_graph(graph))
+    conv, it, hist = pdhg.oracle_run(eng, 1e-300, 1e-300, iters, check_every)
+    return eng, np.array(hist)
+
+
+# ---------------------------------------------------------------------------
+# oracle parity on random inputs, every vector norm pairing, odd sizes
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n,k,norm_u,norm_w,alpha,eps", [
+    (33, 3, "l12", "l1", 0.02, 0.0),
+    (47, 3, "l2", "l2", 0.02, 0.0),
+    (65, 3, "l1", "l1", 0.02, 0.0),
+    (129, 3, "l12", "l1", 0.02, 0.01),
+    (40, 4, "l2", "l1", 0.02, 0.0),
+    (37, 2, "l1", "l2", 0.05, 0.0),
+    (300, 3, "l12", "l1", 0.002, 0.0),
+])
+def test_vector_random_vs_oracle(rng, n, k, norm_u, norm_w, alpha, eps):
+    l0 = _norm_rand(rng, (n, n, k))
+    l1 = _norm_rand(rng, (n, n, k))
+    if k == 3:
+        graph = pk.triangle_graph((1.0, 1.3, 0.8))
+    else:
+        edges = [(i, i + 1) for i in range(k - 1)] + ([(0, k - 1)] if k > 2 else [])
+        graph = pk.TransportGraph(k, edges, np.linspace(0.7, 1.4, len(edges)))
+    cfg = pk.SolverConfig(tau=2.0, norm_u=norm_u, norm_w=norm_w, alpha=alpha, eps_reg=eps,
+                          tol_gap=1e-300, tol_feas=1e-300, max_iters=150, check_every=50)
+    rep, st = pk.solve_vector(pk.VectorDensity(l0), pk.VectorDensity(l1), graph, cfg=cfg)
+    eng, hist = _oracle_vector(l0, l1, graph, cfg, 150, 50)
+    g.hist_close(g.hist_array(rep), hist, 1e-10)
+    assert g.rel_err(st.u.ux, eng.u[:, :, 0]) <= 1e-10
+    assert g.rel_err(st.u.uy, eng.u[:, :, 1]) <= 1e-10
+    assert g.rel_err(st.phi, eng.phi) <= 1e-10
+    assert g.rel_err(st.w.values, eng.w) <= 1e-10
+    assert np.linalg.norm(eng.w) > 0
+
+
+def test_large_grid_few_iterations_vs_oracle():
+    """A 2048^2 rgb instance (the BASELINE C5 family) for 3 iterations."""
+    l0, l1 = synthetic.rgb_disk_pair(2048)
+    graph = pk.triangle_graph()
+    cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", alpha=0.3, tol_gap=1e-300,
+                          tol_feas=1e-300, max_iters=3, check_every=3)
+    rep, st = pk.solve_vector(pk.VectorDensity(l0), pk.VectorDensity(l1), graph, cfg=cfg)
+    eng, hist = _oracle_vector(l0, l1, graph, cfg, 3, 3)
+    g.hist_close(g.hist_array(rep), hist, 1e-10)
+    assert g.rel_err(st.phi, eng.phi) <= 1e-10
+    assert g.rel_err(st.u.ux, eng.u[:, :, 0]) <= 1e-10
+
+
+@pytest.mark.parametrize("k,norm_u,norm_w", [(2, "l1nuc", "l1"), (3, "l1nuc", "l1nuc"),
+                                             (3, "l2", "l1"), (2, "l12", "l2"), (4, "l1nuc", "l1nuc"),
+                                             (4, "l2", "l1")])
+def test_matrix_complex_random_vs_oracle(rng, k, norm_u, norm_w):
+    n = 12
+    a = _rand_herm_psd(rng, n, k)
+    b = _rand_herm_psd(rng, n, k)
+    mats = rng.normal(size=(2, k, k)) + 1j * rng.normal(size=(2, k, k))
+    lind = pk.LindbladSet(0.5 * (mats + np.conj(np.swapaxes(mats, -1, -2))))
+    cfg = pk.SolverConfig(tau=5.0, norm_u=norm_u, norm_w=norm_w, alpha=0.4, tol_gap=1e-300,
+                          tol_feas=1e-300, max_iters=120, check_every=40)
+    rep, st = pk.solve_matrix(a, b, lind, cfg=cfg)
+    eng = pdhg.OracleEngine("matrix", a.values - b.values, n, 5.0, norm_u=norm_u, norm_w=norm_w,
+                            alpha=0.4, chan=lind.matrices, lam_chan=pk.lambda_max_L(lind),
+                            dtype=np.complex128)
+    _, _, hist = pdhg.oracle_run(eng, 1e-300, 1e-300, 120, 40)
+    g.hist_close(g.hist_array(rep), np.array(hist), 1e-9)
+    assert g.rel_err(st.phi, eng.phi) <= 1e-9
+    assert g.rel_err(st.w.values, eng.w) <= 1e-9
+    assert np.linalg.norm(eng.w) > 0
+
+
+# ---------------------------------------------------------------------------
+# reference behaviour (T/test_solver.py)
+# ---------------------------------------------------------------------------
+def test_identical_marginals_immediate(rng):
+    d = pk.normalize(pk.ScalarDensity(rng.random((8, 8))))
+    rep, _ = pk.solve_scalar(d, d)
+    assert rep.converged and rep.iterations == 0
+    assert rep.transport_value == pytest.approx(0.0, abs=1e-12)
+    v = pk.normalize(pk.VectorDensity(rng.random((6, 6, 3))))
+    rep, _ = pk.solve_vector(v, v, pk.triangle_graph())
+    assert rep.converged and rep.iterations == 0
+    m0, _, _ = synthetic.matrix_blob_fixtures(5)
+    rep, _ = pk.solve_matrix(pk.MatrixDensity(m0), pk.MatrixDensity(m0), pk.default_lindblad3())
+    assert rep.converged and rep.transport_value == pytest.approx(0.0, abs=1e-12)
+
+
+def test_mass_mismatch_rejected(rng):
+    a = pk.normalize(pk.ScalarDensity(rng.random((6, 6))))
+    b = pk.ScalarDensity(a.values * 1.5)
+    with pytest.raises(pk.ValidationError):
+        pk.solve_scalar(a, b)
+
+
+def test_ghost_stays_zero(rng):
+    a = pk.normalize(pk.ScalarDensity(rng.random((7, 7))))
+    b = pk.normalize(pk.ScalarDensity(rng.random((7, 7))))
+    _, st = pk.solve_scalar(a, b, cfg=pk.SolverConfig(max_iters=500))
+    assert np.all(st.u.ux[-1, :] == 0) and np.all(st.u.uy[:, -1] == 0)
+    l0, l1 = synthetic.rgb_disk_pair(130)
+    _, st = pk.solve_vector(pk.VectorDensity(l0), pk.VectorDensity(l1), pk.triangle_graph(),
+                            cfg=pk.SolverConfig(max_iters=300, alpha=0.3))
+    assert np.all(st.u.ux[-1] == 0) and np.all(st.u.uy[:, -1] == 0)
+
+
+def test_deterministic_bitwise(rng):
+    a = pk.normalize(pk.VectorDensity(rng.random((70, 70, 3))))
+    b = pk.normalize(pk.VectorDensity(rng.random((70, 70, 3))))
+    cfg = pk.SolverConfig(tau=3.0, max_iters=400, alpha=0.3)
+    r1, s1 = pk.solve_vector(a, b, pk.triangle_graph(), cfg=cfg)
+    r2, s2 = pk.solve_vector(a, b, pk.triangle_graph(), cfg=cfg)
+    assert r1.transport_value == r2.transport_value and r1.iterations == r2.iterations
+    assert np.array_equal(s1.phi, s2.phi) and np.array_equal(s1.u.ux, s2.u.ux)
+    assert np.array_equal(s1.w.values, s2.w.values)
+
+
+def test_nonconvergence_reported(rng):
+    a = pk.normalize(pk.ScalarDensity(rng.random((8, 8))))
+    b = pk.normalize(pk.ScalarDensity(rng.random((8, 8))))
+    rep, _ = pk.solve_scalar(a, b, cfg=pk.SolverConfig(max_iters=5))
+    assert not rep.converged and rep.iterations == 5
+
+
+def test_matrix_structure_exact():
+    m0, m1, _ = synthetic.matrix_blob_fixtures(8)
+    cfg = pk.SolverConfig(tau=10.0, norm_u="l2", norm_w="l1")
+    rep, st = pk.solve_matrix(pk.MatrixDensity(m0), pk.MatrixDensity(m1), pk.default_lindblad3(),
+                              cfg=cfg)
+    assert rep.converged
+    phi = st.phi
+    assert np.array_equal(phi, np.conj(np.swapaxes(phi, -1, -2)))
+    wv = st.w.values
+    assert np.array_equal(wv, -np.conj(np.swapaxes(wv, -1, -2)))
+    ux = st.u.ux
+    assert np.array_equal(ux, np.conj(np.swapaxes(ux, -1, -2)))
+    res = [h.residual for h in rep.history if np.isfinite(h.residual)]
+    assert all(r >= -1e-9 * max(res[0], 1.0) for r in res)
+    for x, y in zip(res, res[1:]):
+        assert y <= x * (1 + 1e-9) + 1e-15
+
+
+def test_channel_swap_costs_alpha():
+    v0 = np.zeros((4, 4, 3))
+    v0[1, 1, 0] = 1.0
+    v1 = np.zeros((4, 4, 3))
+    v1[1, 1, 1] = 1.0
+    cfg = pk.SolverConfig(norm_u="l1", norm_w="l1")
+    rep, _ = pk.solve_vector(pk.VectorDensity(v0), pk.VectorDensity(v1), pk.triangle_graph(), cfg=cfg)
+    assert rep.converged and rep.transport_value == pytest.approx(1.0, rel=0.02)
+
+
+def test_regularized_nuclear_rejected():
+    m0, m1, _ = synthetic.matrix_blob_fixtures(5)
+    cfg = pk.SolverConfig(eps_reg=0.1, norm_u="l1nuc", norm_w="l1")
+    with pytest.raises(pk.UnsupportedNormError):
+        pk.solve_matrix(pk.MatrixDensity(m0), pk.MatrixDensity(m1), pk.default_lindblad3(), cfg=cfg)
+
+
+# ---------------------------------------------------------------------------
+# metric helpers on the device vs the oracle
+# ---------------------------------------------------------------------------
+def test_duality_gap_and_residual_vs_oracle(rng):
+    n = 20
+    a = pk.normalize(pk.VectorDensity(rng.random((n, n, 3))))
+    b = pk.normalize(pk.VectorDensity(rng.random((n, n, 3))))
+    gph = pk.triangle_graph()
+    states = []
+    for iters in (40, 41):
+        _, st = pk.solve_vector(a, b, gph, cfg=pk.SolverConfig(max_iters=iters, check_every=1000,
+                                                                alpha=0.3))
+        states.append(st)
+    mu, nu, tau = pk.step_sizes_vector(pk.GridSpec(n), gph, 1.0)
+    r = pk.residual_Rk(states[0], states[1], mu, nu, tau, graph=gph)
+    eng = pdhg.OracleEngine("vector", a.values - b.values, n, 1.0, norm_w="l1", alpha=0.3,
+                            chan=gph.coefficients(), lam_chan=pk.lambda_max_graph(gph))
+    eng.u = np.stack([states[1].u.ux, states[1].u.uy], axis=2)
+    eng.w = states[1].w.values
+    eng.phi = states[1].phi
+    ref = eng.residual_from(np.stack([states[0].u.ux, states[0].u.uy], axis=2),
+                            states[0].w.values, states[0].phi)
+    assert r == pytest.approx(ref, rel=1e-10, abs=1e-18)
+    assert r >= 0
+    cfg = pk.SolverConfig(alpha=0.3)
+    got = pk.duality_gap(states[1], a, b, cfg, graph=gph)
+    want = eng.evaluate()
+    np.testing.assert_allclose(got, want, rtol=1e-10, atol=1e-15)
+    zero = pk.SolverState(u=states[1].u, w=states[1].w, phi=np.zeros_like(states[1].phi),
+                          iteration=0, residual=0.0, primal_value=0.0, dual_value=0.0,
+                          gap_ratio=0.0, feas_residual=0.0)
+    p, d, gap, f = pk.duality_gap(zero, a, b, cfg, graph=gph)
+    assert d == 0.0 and gap == pytest.approx(1.0)
+
+
+# ---------------------------------------------------------------------------
+# row-slab decomposition on one GPU: P engines stepped in lockstep with halo
+# copies must reproduce the single-slab iterates bit for bit
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("P,n", [(2, 64), (3, 101), (4, 256)])
+def test_local_slabs_bit_identical(P, n):
+    l0, l1 = synthetic.rgb_disk_pair(n)
+    gph = pk.triangle_graph()
+    cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", alpha=0.3)
+    whole = build_engine("vector", n, cfg, graph=gph)
+    whole.set_marginals(l0, l1)
+    whole.step(57)
+    ref = whole.step_check()
+    ux, uy, w, phi = whole.get_state()
+    whole.close()
+    bounds = np.linspace(0, n, P + 1).astype(int)
+    slabs = []
+    stream = None
+    for r in range(P):
+        e = build_engine("vector", n, cfg, graph=gph, rows=(bounds[r], bounds[r + 1]), stream=stream)
+        stream = e.stream
+        e.set_marginals(l0[bounds[r]:bounds[r + 1]], l1[bounds[r]:bounds[r + 1]])
+        slabs.append(e)
+    dn = float(np.sqrt(sum(e.diff_norm ** 2 for e in slabs)))
+    for e in slabs:
+        e.diff_norm = dn
+    for it in range(58):
+        for e in slabs:
+            e.sweep(check=(it == 57))
+        exchange_local(slabs)
+    raws = [e.raw(with_residual=True) for e in slabs]
+    tot = np.sum([r[:12] for r in raws], axis=0)
+    mx = np.max([r[12:] for r in raws], axis=0)
+    out = slabs[0].finalize(np.concatenate([tot, mx]))
+    got = [e.get_state() for e in slabs]
+    for q, ref_arr in enumerate((ux, uy, w, phi)):
+        cat = np.concatenate([s[q] for s in got], axis=0)
+        assert np.array_equal(cat, ref_arr), q
+    np.testing.assert_allclose(out, ref, rtol=1e-12)
+    for e in reversed(slabs):  # slab 0 owns the shared stream
+        e.close()
