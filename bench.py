@@ -302,10 +302,13 @@ def run_ours(args):
                 "l2": f"no flush needed: per-GPU iterate pair {state_gb:.1f} GB >> 126 MB L2",
                 "tile": [info["tile_cols"], info["tile_rows"]],
                 "regs": [info["regs_plain"], info["regs_check"]],
+                "tma_stages": info["tma_stages"], "smem_per_cta": info["smem_bytes"],
                 "final_primal": last[0], "final_gap": last[2]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "sweep_kernel (fused flux+potential update)",
+                         "kernel": ("sweep_tma_kernel (TMA-streamed fused PDHG iteration)"
+                                    if info["tma_stages"] else
+                                    "sweep_kernel (register-streamed fused PDHG iteration)"),
                          "bytes_per_launch": balg, "avg_launch_ms": sweep_ms,
                          "step_frac": value / world * bytes_per_cell(args.precision) / 1e9 / peak,
                          "peak_source": peak_src},

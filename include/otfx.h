@@ -109,6 +109,8 @@ typedef struct {
   int32_t tile_cols, tile_rows, grid_x, grid_y; /* sweep launch geometry */
   int32_t regs_plain, regs_check;               /* registers per thread */
   int32_t graphs;        /* CUDA graphs in use */
+  int32_t tma_stages;    /* TMA ring depth of the streamed sweep (0: register sweep) */
+  int32_t smem_bytes;    /* dynamic shared memory per sweep CTA */
 } otfx_engine_info;
 
 int otfx_abi_version(void);

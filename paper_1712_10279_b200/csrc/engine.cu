@@ -1,6 +1,8 @@
 // Host runtime of the otfx engine: device memory, layout conversion, the
 // iteration / check / run loops (CUDA graphs), halo exchange (local copies or
 // NCCL over NVLink), and the extern "C" ABI of include/otfx.h.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -259,6 +261,10 @@ struct otfx_engine {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   void* d_halo = nullptr;  // send/recv buffers
+  // TMA-streamed sweep
+  bool use_tma = false;
+  otfx::StageLayout L{};
+  otfx::TmaSet maps[2];
   // policy dispatch
   const otfx::Ops<double>* ops64 = nullptr;
   const otfx::Ops<float>* ops32 = nullptr;
@@ -320,10 +326,76 @@ const Ops<float>* ops_of<float>(otfx_engine* e) { return e->ops32; }
 
 template <typename T>
 static void launch_sweep(otfx_engine* e, bool check) {
-  SweepArgs<T> a = make_args<T>(e, e->cur);
-  CK(ops_of<T>(e)->sweep(a, dim3(e->gx, e->gy), dim3(e->TX), check ? e->smem_check : e->smem_plain,
-                         e->stream, check));
+  if (e->use_tma) {
+    TmaSweepArgs<T> g;
+    g.s = make_args<T>(e, e->cur);
+    g.L = e->L;
+    CK(ops_of<T>(e)->sweep_tma(g, e->maps[e->cur], dim3(e->gx, e->gy), dim3(32 * (e->L.cw + 1)),
+                               e->stream, check));
+  } else {
+    SweepArgs<T> a = make_args<T>(e, e->cur);
+    CK(ops_of<T>(e)->sweep(a, dim3(e->gx, e->gy), dim3(e->TX),
+                           check ? e->smem_check : e->smem_plain, e->stream, check));
+  }
   e->cur ^= 1;
+}
+
+// ---- TMA descriptors ------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    require(q == cudaDriverEntryPointSuccess && p != nullptr, OTFX_ECUDA,
+            "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D view (cols = n, rows = rows_alloc, planes) of a group of planes; one box
+// = L.tw columns x 1 row x all planes; columns outside [0, n) read as zero
+static void make_map(otfx_engine* e, CUtensorMap* m, void* base, int planes) {
+  memset(m, 0, sizeof(*m));
+  if (planes <= 0) return;
+  require(planes <= 256, OTFX_EUNSUPPORTED, "too many planes for one TMA box");
+  cuuint64_t dims[3] = {cuuint64_t(e->d.n), cuuint64_t(e->rows_alloc), cuuint64_t(planes)};
+  cuuint64_t strides[2] = {cuuint64_t(e->pitch) * e->elem, cuuint64_t(e->plane) * e->elem};
+  cuuint32_t box[3] = {cuuint32_t(e->L.tw), 1u, cuuint32_t(planes)};
+  cuuint32_t es[3] = {1u, 1u, 1u};
+  CUresult r = tensor_map_encoder()(
+      m, e->elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base,
+      dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  require(r == CUDA_SUCCESS, OTFX_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+}
+
+static int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
+// shared-memory plan of the TMA sweep; returns false when it cannot fit
+static bool plan_stages(otfx_engine* e, int S) {
+  StageLayout& L = e->L;
+  require(S >= 3 && S <= 8, OTFX_EINVAL, "TMA ring depth must be in [3, 8]");
+  L.cw = 4;
+  L.tile = 31 * L.cw;  // 124: a multiple of 16 bytes' worth of columns for fp32 and fp64
+  L.h = 16 / e->elem;
+  L.tw = L.tile + 2 * L.h;
+  L.S = S;
+  const int row = L.tw * e->elem;
+  const int bu = 2 * e->NP * row, bw = e->NWact * row, bd = e->NP * row, bp = e->NP * row;
+  L.off_w = round_up(bu, 128);
+  L.off_d = L.off_w + round_up(bw, 128);
+  L.off_p = L.off_d + round_up(bd, 128);
+  L.stage_bytes = L.off_p + round_up(bp, 128);
+  L.bytes_full = bu + bw + bd + bp;
+  L.bytes_flux = bu + bp;
+  L.bytes_phi = bp;
+  L.off_stages = 128;
+  L.off_xchg = L.off_stages + S * L.stage_bytes;
+  L.off_red = round_up(L.off_xchg, 16);
+  L.total = L.off_red + 32 * 4 * 8;
+  return L.total <= 227 * 1024;
 }
 
 static void launch_sweep(otfx_engine* e, bool check) {
@@ -825,6 +897,8 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   // sweep geometry: TX columns per CTA, R rows per CTA, >= ~4 CTAs per SM
   const int n = d->n;
   e->TX = env_int("OTFX_TILE_COLS", n > 64 ? 128 : (n > 32 ? 64 : 32));
+  require(e->TX % 32 == 0 && e->TX >= 32 && e->TX <= 128, OTFX_EINVAL,
+          "tile columns must be 32, 64, 96 or 128");
   e->gx = (n + e->TX - 1) / e->TX;
   const int want = 148 * 4;
   int gy = (want + e->gx - 1) / e->gx;
@@ -837,7 +911,27 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   e->smem_plain = ((2 * sw + 15) & ~size_t(15)) + 32 * 4 * sizeof(double);
   e->smem_check = ((3 * sw + 15) & ~size_t(15)) + 32 * 4 * sizeof(double);
   e->ex = (n + 127) / 128;
-  e->ey = e->rows;
+  e->ey = std::min(e->rows, std::max(1, 2048 / e->ex));
+  // TMA-streamed sweep: ring depth 4 (3 if that keeps two CTAs per SM)
+  e->use_tma = env_int("OTFX_TMA", 1) != 0;
+  if (e->use_tma) {
+    int S = env_int("OTFX_STAGES", 0);
+    if (S <= 0) {
+      S = 4;
+      plan_stages(e, S);
+      if (e->L.total > 110 * 1024) S = 3;
+    }
+    e->use_tma = plan_stages(e, std::max(3, S));
+  }
+  if (e->use_tma) {
+    e->gx = (n + e->L.tile - 1) / e->L.tile;
+    const int want2 = 148 * 4;
+    int gy2 = (want2 + e->gx - 1) / e->gx;
+    int R2 = (e->rows + gy2 - 1) / gy2;
+    R2 = std::max(4, std::min(128, R2));
+    e->R = env_int("OTFX_TILE_ROWS", R2);
+    e->gy = (e->rows + e->R - 1) / e->R;
+  }
 
   // staging: up to 64 MB, at least two grid rows of the widest record
   const int max_rec = std::max(2 * e->K * e->K * std::max(1, d->ell) * 2, 16);
@@ -876,6 +970,14 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   e->d_pack_part = reinterpret_cast<double*>(e->mem + o_pack);
   e->d_halo = e->mem + o_halo;
   e->d_stage = reinterpret_cast<double*>(e->mem + o_stage);
+  if (e->use_tma) {
+    for (int st = 0; st < 2; ++st) {
+      make_map(e, &e->maps[st].u, e->u[st], 2 * NP);
+      make_map(e, &e->maps[st].w, e->w[st], e->NWact);
+      make_map(e, &e->maps[st].phi, e->phi[st], NP);
+      make_map(e, &e->maps[st].diff, e->diff, NP);
+    }
+  }
   CK(cudaMallocHost(&e->h_raw, 64 * sizeof(double)));
   CK(cudaMallocHost(&e->h_pack_part, kPackBlocks * 3 * sizeof(double)));
   CK(e->ops64 ? e->ops64->prepare() : e->ops32->prepare());
@@ -975,13 +1077,19 @@ int otfx_engine_get_info(otfx_engine* e, otfx_engine_info* info) {
   info->nws = e->NWS;
   info->lmax = e->LMAX;
   info->pitch = e->pitch;
-  info->tile_cols = e->TX;
+  info->tile_cols = e->use_tma ? e->L.tile : e->TX;
   info->tile_rows = e->R;
   info->grid_x = e->gx;
   info->grid_y = e->gy;
   info->regs_plain = e->ops64 ? e->ops64->sweep_regs(false) : e->ops32->sweep_regs(false);
   info->regs_check = e->ops64 ? e->ops64->sweep_regs(true) : e->ops32->sweep_regs(true);
   info->graphs = e->use_graphs ? 1 : 0;
+  info->tma_stages = e->use_tma ? e->L.S : 0;
+  info->smem_bytes = e->use_tma ? e->L.total : int(e->smem_plain);
+  if (e->use_tma) {
+    info->regs_plain = e->ops64 ? e->ops64->tma_regs(false) : e->ops32->tma_regs(false);
+    info->regs_check = e->ops64 ? e->ops64->tma_regs(true) : e->ops32->tma_regs(true);
+  }
   API_END
 }
 

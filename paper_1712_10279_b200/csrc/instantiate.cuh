@@ -3,6 +3,7 @@
 
 #include "ops.h"
 #include "sweep.cuh"
+#include "sweep_tma.cuh"
 
 namespace otfx {
 
@@ -12,8 +13,28 @@ struct OpsFor {
     cudaError_t e = cudaFuncSetAttribute(sweep_kernel<P, T, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(sweep_kernel<P, T, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    e = cudaFuncSetAttribute(sweep_kernel<P, T, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(sweep_tma_kernel<P, T, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(sweep_tma_kernel<P, T, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  }
+  static cudaError_t sweep_tma(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
+                               cudaStream_t s, bool check) {
+    if (check)
+      sweep_tma_kernel<P, T, true><<<g, b, a.L.total, s>>>(a, m);
+    else
+      sweep_tma_kernel<P, T, false><<<g, b, a.L.total, s>>>(a, m);
+    return cudaGetLastError();
+  }
+  static int tma_regs(bool check) {
+    cudaFuncAttributes at;
+    if (check) cudaFuncGetAttributes(&at, sweep_tma_kernel<P, T, true>);
+    else cudaFuncGetAttributes(&at, sweep_tma_kernel<P, T, false>);
+    return at.numRegs;
   }
   static cudaError_t sweep(const SweepArgs<T>& a, dim3 g, dim3 b, size_t smem, cudaStream_t s,
                            bool check) {
@@ -39,7 +60,8 @@ struct OpsFor {
   }
   static const Ops<T>* table(int kind) {
     static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
-                             P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &regs};
+                             P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &sweep_tma,
+                             &regs,    &tma_regs};
     return &o;
   }
 };

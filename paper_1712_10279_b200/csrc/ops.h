@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "sweep_tma.cuh"
 
 namespace otfx {
 
@@ -20,7 +21,10 @@ struct Ops {
                        bool check);
   cudaError_t (*evaluate)(const SweepArgs<T>& a, dim3 grid, dim3 block, cudaStream_t s);
   cudaError_t (*residual)(const SweepArgs<T>& a, dim3 grid, dim3 block, cudaStream_t s);
+  cudaError_t (*sweep_tma)(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 grid, dim3 block,
+                           cudaStream_t s, bool check);
   int (*sweep_regs)(bool check);
+  int (*tma_regs)(bool check);
 };
 
 // registries, one per instantiation unit

@@ -314,12 +314,11 @@ __global__ void __launch_bounds__(128) evaluate_kernel(const __grid_constant__ S
   constexpr int NWA = P::NWA;
   __shared__ double sred[32 * 8];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = A.row_begin + blockIdx.y;
   const int n = A.n;
   const int64_t pl = A.plane;
   double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // PU PW SU2 SW2 SCON SPHID PENU PENW
   double mx[2] = {0.0, 0.0};
-  if (j < n && i < A.row_end) {
+  for (int i = A.row_begin + blockIdx.y; j < n && i < A.row_end; i += gridDim.y) {
     const int64_t o = cell_off(A, i, j);
     T u[2][NP], ph[NP], df[NP], w[NWA];
 #pragma unroll
@@ -333,12 +332,12 @@ __global__ void __launch_bounds__(128) evaluate_kernel(const __grid_constant__ S
 #pragma unroll
       for (int e = 0; e < NWA; ++e) w[e] = (e < A.ell * P::NWS) ? ldg(A.a.w + e * pl + o) : T(0);
     }
-    s[0] = P::norm_u(u, A.norm_u);
+    s[0] += P::norm_u(u, A.norm_u);
     double su = 0.0;
 #pragma unroll
     for (int c = 0; c < NP; ++c)
       su += P::wp(c) * (double(u[0][c]) * double(u[0][c]) + double(u[1][c]) * double(u[1][c]));
-    s[2] = su;
+    s[2] += su;
     // constraint residual: div u - diff + div_c w
     T con[NP];
     const int64_t oxm = cell_off(A, i - 1, j), oym = o - 1;
@@ -351,11 +350,11 @@ __global__ void __launch_bounds__(128) evaluate_kernel(const __grid_constant__ S
       con[c] = d * A.inv_dx - df[c];
     }
     if (P::HAS_W) {
-      s[1] = P::norm_w(w, A.norm_w);  // inactive channel blocks are zero
+      s[1] += P::norm_w(w, A.norm_w);  // inactive channel blocks are zero
       double sw = 0.0;
 #pragma unroll
       for (int e = 0; e < NWA; ++e) sw += P::ww(e) * double(w[e]) * double(w[e]);
-      s[3] = sw;
+      s[3] += sw;
       T dv[NP];
       P::div_c(w, dv, A);
 #pragma unroll
@@ -367,8 +366,8 @@ __global__ void __launch_bounds__(128) evaluate_kernel(const __grid_constant__ S
       sc += P::wp(c) * double(con[c]) * double(con[c]);
       sp += P::wp(c) * double(ph[c]) * double(df[c]);
     }
-    s[4] = sc;
-    s[5] = sp;
+    s[4] += sc;
+    s[5] += sp;
     // dual norms of grad phi and grad_c phi
     T g[2][NP];
     const bool hx = i + 1 < n, hy = j + 1 < n;
@@ -411,11 +410,10 @@ __global__ void __launch_bounds__(128) residual_kernel(const __grid_constant__ S
   constexpr int NWA = P::NWA;
   __shared__ double sred[32 * 4];
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = A.row_begin + blockIdx.y;
   const int n = A.n;
   const int64_t pl = A.plane;
   double s[4] = {0, 0, 0, 0};
-  if (j < n && i < A.row_end) {
+  for (int i = A.row_begin + blockIdx.y; j < n && i < A.row_end; i += gridDim.y) {
     const int64_t o = cell_off(A, i, j), oxm = cell_off(A, i - 1, j);
     auto du = [&](int comp, int64_t off) { return A.b.u[comp * pl + off] - A.a.u[comp * pl + off]; };
     T cross[NP];

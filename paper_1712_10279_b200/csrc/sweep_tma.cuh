@@ -1,0 +1,310 @@
+// TMA-streamed, warp-specialised variant of the fused PDHG sweep (same
+// arithmetic as sweep.cuh, same results bit for bit).
+//
+// The register-streaming sweep issues its row loads and immediately waits on
+// them, and a CTA-wide barrier per row ties its warps together, so memory
+// parallelism per SM is bounded by the warps that happen to be in their load
+// phase.  Here one producer warp per CTA drives a ring of S row stages in
+// shared memory: one 3-D TMA box per field group (u: 2NP planes, w, diff,
+// phi) of TW = tile + 2h columns (cols c0-h .. c0+tile+h-1, zero-filled outside
+// the grid by the tensor map; h makes the box start 16-byte aligned, which the
+// TMA unit requires) lands on a "full" mbarrier; every consumer warp
+// releases a stage through an "empty" mbarrier when it is done with it.
+// Consumer warps overlap by one column: lane 0 of each warp only computes
+// the spatial flux of the column left of the warp's 31 output columns, and
+// ubar_y(i, j-1) reaches lane l from lane l-1 by a warp shuffle.  Consumers
+// therefore never wait for each other (no block barrier in the row loop) and
+// the redundant work is 1/32 of the flux.
+//
+// Stage q of a CTA holds global row qbase + q with qbase = gr0 - 1:
+//   q = 0            halo row gr0-1: u, phi          (skipped when gr0 == 0)
+//   q = 1 .. R       rows gr0 .. gr1-1: u, w, diff, phi
+//   q = R + 1        row gr1: phi only               (skipped when gr1 == n)
+// Skipped stages complete their mbarrier with a plain arrive so the phase
+// bookkeeping (parity = (q / S) & 1) stays uniform.
+#pragma once
+
+#include "sweep.cuh"
+#include "tma.cuh"
+
+namespace otfx {
+
+struct alignas(64) TmaSet {
+  CUtensorMap u, w, phi, diff;
+};
+
+struct StageLayout {
+  int cw;          // consumer warps per CTA (a producer warp follows them)
+  int tile;        // output columns per CTA = 31 * cw
+  int h;           // halo columns staged each side: 16 B worth (TMA needs the box
+                   // start column 16-byte aligned), 2 for fp64, 4 for fp32
+  int tw;          // staged columns = tile + 2h (cols c0-h .. c0+tile+h-1)
+  int S;           // ring depth
+  int off_w, off_d, off_p;  // byte offsets inside a stage
+  int stage_bytes;
+  int bytes_full, bytes_flux, bytes_phi;  // expect-tx per stage kind
+  int off_stages, off_xchg, off_red;      // byte offsets in dynamic smem
+  int total;
+};
+
+template <typename T>
+struct TmaSweepArgs {
+  SweepArgs<T> s;
+  StageLayout L;
+};
+
+template <class P, typename T, bool CHECK>
+__global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ TmaSweepArgs<T> G,
+                                                       const __grid_constant__ TmaSet M) {
+  constexpr int NP = P::NP;
+  constexpr int NWA = P::NWA;
+  const SweepArgs<T>& A = G.s;
+  const StageLayout& L = G.L;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [S]
+  uint64_t* empty = full + 8;                          // [S]
+  double* sred = reinterpret_cast<double*>(smem + L.off_red);
+
+  const int CW = L.cw;
+  const int TW = L.tw;
+  const int S = L.S;
+  const int t = threadIdx.x;
+  const int warp = t >> 5, lane = t & 31;
+  const bool producer = warp >= CW;
+  const int c0 = blockIdx.x * L.tile;
+  const int sc = L.h + 31 * warp + lane - 1;  // staged column index of this thread's column
+  const int j = c0 - L.h + sc;                // = c0 + 31 warp + lane - 1
+  const int n = A.n;
+  const bool out = !producer && lane > 0 && j < n;  // lane 0 is the overlap column
+  const bool hasy = j + 1 < n;
+  const int gr0 = A.row_begin + blockIdx.y * A.rows_per_block;
+  const int gr1 = min(gr0 + A.rows_per_block, A.row_end);
+  const int qbase = gr0 - 1;
+  const int qmax = gr1 - qbase;  // index of the phi-only tail stage
+  const int64_t pl = A.plane;
+  const int nwp = A.ell * P::NWS;
+
+  auto stage = [&](int q) -> unsigned char* {
+    return smem + L.off_stages + (q % S) * L.stage_bytes;
+  };
+  auto U = [&](int q, int p, int col) -> T {
+    return reinterpret_cast<const T*>(stage(q))[p * TW + col];
+  };
+  auto Wv = [&](int q, int p, int col) -> T {
+    return reinterpret_cast<const T*>(stage(q) + L.off_w)[p * TW + col];
+  };
+  auto Dv = [&](int q, int p, int col) -> T {
+    return reinterpret_cast<const T*>(stage(q) + L.off_d)[p * TW + col];
+  };
+  auto PH = [&](int q, int p, int col) -> T {
+    return reinterpret_cast<const T*>(stage(q) + L.off_p)[p * TW + col];
+  };
+
+  if (t == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (producer) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const int cx = c0 - L.h;
+      for (int q = 0; q <= qmax; ++q) {
+        const int slot = q % S;
+        if (q >= S) mbar_wait(&empty[slot], ((q / S) - 1) & 1);
+        uint64_t* bar = &full[slot];
+        const int r = qbase + q;
+        const int lrow = r - A.row_begin + 1;
+        unsigned char* st = stage(q);
+        if (q == 0 || q == qmax) {
+          const bool load = (q == 0) ? (gr0 > 0) : (r < n);
+          if (!load) {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+            continue;
+          }
+          if (q == 0) {
+            mbar_expect_tx(bar, L.bytes_flux);
+            tma_load_3d(st, &M.u, bar, cx, lrow, 0);
+          } else {
+            mbar_expect_tx(bar, L.bytes_phi);
+          }
+          tma_load_3d(st + L.off_p, &M.phi, bar, cx, lrow, 0);
+        } else {
+          mbar_expect_tx(bar, L.bytes_full);
+          tma_load_3d(st, &M.u, bar, cx, lrow, 0);
+          if (P::HAS_W) tma_load_3d(st + L.off_w, &M.w, bar, cx, lrow, 0);
+          tma_load_3d(st + L.off_d, &M.diff, bar, cx, lrow, 0);
+          tma_load_3d(st + L.off_p, &M.phi, bar, cx, lrow, 0);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    auto wait_full = [&](int q) { mbar_wait(&full[q % S], (q / S) & 1); };
+    auto release = [&](int q) {
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[q % S]))
+                     : "memory");
+    };
+    T uxb_prev[NP], dux_prev[NP];
+#pragma unroll
+    for (int c = 0; c < NP; ++c) {
+      uxb_prev[c] = T(0);
+      dux_prev[c] = T(0);
+    }
+    // halo row gr0-1: ubar_x(gr0-1, j) from the read-only iterate
+    wait_full(0);
+    if (gr0 > 0) {
+      wait_full(1);
+      T pm[NP], px[NP], py[NP], uo[2][NP], un[2][NP];
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        pm[c] = PH(0, c, sc);
+        py[c] = PH(0, c, sc + 1);
+        px[c] = PH(1, c, sc);
+        uo[0][c] = U(0, c, sc);
+        uo[1][c] = U(0, NP + c, sc);
+      }
+      Cell<P, T>::flux(pm, px, py, true, hasy, uo, un, A);
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        uxb_prev[c] = (un[0][c] + un[0][c]) - uo[0][c];
+        dux_prev[c] = un[0][c] - uo[0][c];
+      }
+    }
+    release(0);
+
+    for (int i = gr0; i < gr1; ++i) {
+      const int q = i - qbase;
+      const bool hasx = i + 1 < n;
+      wait_full(q);
+      wait_full(q + 1);
+      T phc[NP], un[2][NP], ub[2][NP], uo[2][NP], lub[NP], ldu[NP];
+      {
+        T phx[NP], phy[NP];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          phc[c] = PH(q, c, sc);
+          phy[c] = PH(q, c, sc + 1);
+          phx[c] = PH(q + 1, c, sc);
+          uo[0][c] = U(q, c, sc);
+          uo[1][c] = U(q, NP + c, sc);
+        }
+        Cell<P, T>::flux(phc, phx, phy, hasx, hasy, uo, un, A);
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          ub[0][c] = (un[0][c] + un[0][c]) - uo[0][c];
+          ub[1][c] = (un[1][c] + un[1][c]) - uo[1][c];
+          // ubar_y / du_y of the left neighbour (i, j-1) from lane - 1
+          lub[c] = __shfl_up_sync(0xffffffffu, ub[1][c], 1);
+          if (CHECK) ldu[c] = __shfl_up_sync(0xffffffffu, un[1][c] - uo[1][c], 1);
+        }
+      }
+      T df[NP], wo[NWA];
+#pragma unroll
+      for (int c = 0; c < NP; ++c) df[c] = Dv(q, c, sc);
+      if (P::HAS_W) {
+#pragma unroll
+        for (int e = 0; e < NWA; ++e) wo[e] = e < nwp ? Wv(q, e, sc) : T(0);
+      }
+      release(q);  // stage q fully consumed (stage q+1 stays for the next row)
+      if (out) {
+        const int64_t o = cell_off(A, i, j);
+        T rhs[NP];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          T d = ub[0][c];
+          if (i > 0) d = d - uxb_prev[c];
+          d = d + ub[1][c];
+          if (j > 0) d = d - lub[c];
+          d = d * A.inv_dx;
+          rhs[c] = d - df[c];
+        }
+        T wn[NWA], dwv[NWA];
+        if (P::HAS_W) {
+          T g[NWA];
+          P::grad_c(phc, g, A);
+#pragma unroll
+          for (int e = 0; e < NWA; ++e) wn[e] = g[e] * A.nu + wo[e];
+          P::prox_w(wn, A);
+          T wb[NWA], dv[NP];
+#pragma unroll
+          for (int e = 0; e < NWA; ++e) {
+            wb[e] = (wn[e] + wn[e]) - wo[e];
+            dwv[e] = wn[e] - wo[e];
+          }
+          P::div_c(wb, dv, A);
+#pragma unroll
+          for (int c = 0; c < NP; ++c) rhs[c] = rhs[c] + dv[c];
+        }
+        T phnew[NP];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          rhs[c] = rhs[c] * A.tau;
+          phnew[c] = phc[c] + rhs[c];
+        }
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          A.b.u[c * pl + o] = un[0][c];
+          A.b.u[(NP + c) * pl + o] = un[1][c];
+          A.b.phi[c * pl + o] = phnew[c];
+        }
+        if (P::HAS_W) {
+#pragma unroll
+          for (int e = 0; e < NWA; ++e)
+            if (e < nwp) A.b.w[e * pl + o] = wn[e];
+        }
+        if (CHECK) {
+          T cross[NP];
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            const T dx = un[0][c] - uo[0][c];
+            const T dy = un[1][c] - uo[1][c];
+            acc[0] += P::wp(c) * (double(dx) * double(dx) + double(dy) * double(dy));
+            T d = dx;
+            if (i > 0) d = d - dux_prev[c];
+            d = d + dy;
+            if (j > 0) d = d - ldu[c];
+            cross[c] = d * A.inv_dx;
+          }
+          if (P::HAS_W) {
+            T dv[NP];
+            P::div_c(dwv, dv, A);
+#pragma unroll
+            for (int c = 0; c < NP; ++c) cross[c] = cross[c] + dv[c];
+#pragma unroll
+            for (int e = 0; e < NWA; ++e) acc[1] += P::ww(e) * double(dwv[e]) * double(dwv[e]);
+          }
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            const T dp = phnew[c] - phc[c];
+            acc[2] += P::wp(c) * double(dp) * double(dp);
+            acc[3] += P::wp(c) * double(dp) * double(cross[c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        uxb_prev[c] = ub[0][c];
+        if (CHECK) dux_prev[c] = un[0][c] - uo[0][c];
+      }
+    }
+  }
+
+  if (CHECK) {
+    block_sum<4>(acc, sred);
+    if (t == 0) {
+      double* dst = A.partials + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * 4;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) dst[s] = acc[s];
+    }
+  }
+}
+
+}  // namespace otfx

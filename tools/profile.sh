@@ -12,6 +12,6 @@ mkdir -p gpurun_out
 $CMD > gpurun_out/${TAG}_plain.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:sweep -s 3 -c 1 \
     -o gpurun_out/${TAG}_sweep $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo profile done
