@@ -359,7 +359,25 @@ def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn):
     sec = float(t[0])
     cells = float(n) * n
     rows_cells = float(r1 - r0) * n
-    return {"value": cells * M / sec, "unit": UNIT,
+    breakdown = None
+    if world == 1:
+        # one instrumented solve through the engine API (not part of the timed steps)
+        from paper_1712_10279_b200.solver import build_engine
+
+        tb = [time.perf_counter()]
+        eng = build_engine("vector", n, cfg, graph=graph, precision=args.precision, device=local)
+        tb.append(time.perf_counter())
+        eng.set_marginals(l0, l1)
+        tb.append(time.perf_counter())
+        eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+        tb.append(time.perf_counter())
+        eng.get_state()
+        tb.append(time.perf_counter())
+        eng.close()
+        tb.append(time.perf_counter())
+        breakdown = dict(zip(["create", "upload", "run", "download", "destroy"],
+                             [round(b - a, 4) for a, b in zip(tb, tb[1:])]))
+    return {"value": cells * M / sec, "unit": UNIT, "breakdown_s": breakdown,
             "h2d_bytes_per_step": int(2 * rows_cells * K_CH * 8),
             "d2h_bytes_per_step": int(rows_cells * (2 * K_CH + ELL + K_CH) * 8),
             "iterations_per_step": M, "seconds_per_step": sec,

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -472,6 +473,11 @@ static void exchange_nccl(otfx_engine* e) {
                          cudaMemcpyDeviceToDevice, e->stream));
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 static void enqueue_plain(otfx_engine* e, int64_t count) {
   for (int64_t q = 0; q < count; ++q) {
     launch_sweep(e, false);
@@ -481,7 +487,9 @@ static void enqueue_plain(otfx_engine* e, int64_t count) {
 
 static void run_plain(otfx_engine* e, int64_t count) {
   if (count <= 0) return;
-  if (!e->use_graphs || count < 3) {
+  // NCCL halo exchanges stay outside graph capture unless explicitly enabled
+  const bool graphs = e->use_graphs && (e->nranks == 1 || env_int("OTFX_NCCL_GRAPHS", 0) != 0);
+  if (!graphs || count < 3) {
     enqueue_plain(e, count);
     return;
   }
@@ -755,54 +763,122 @@ static void pack_chunk(otfx_engine* e, const double* s0, const double* s1, int64
   CK(cudaGetLastError());
 }
 
+// ---- pinned staging pool shared by all engines of the process -------------
+// Host <-> device transfers go through two pinned slots per direction so the
+// multi-threaded host memcpy of chunk k overlaps the DMA of chunk k-1.
+struct PinnedPool {
+  static constexpr size_t kSlot = size_t(32) << 20;  // bytes per slot
+  unsigned char* buf = nullptr;                        // 4 slots: 2 x (in0, in1)
+  cudaEvent_t ev[2]{};
+  std::mutex mu;
+};
+
+static PinnedPool& pinned_pool() {
+  static PinnedPool* p = [] {
+    PinnedPool* q = new PinnedPool();
+    CK(cudaMallocHost(&q->buf, 4 * PinnedPool::kSlot));
+    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&q->ev[i], cudaEventDisableTiming));
+    return q;
+  }();
+  return *p;
+}
+
+static void par_copy(void* dst, const void* src, size_t bytes) {
+  const size_t grain = size_t(4) << 20;
+  const long nblk = long((bytes + grain - 1) / grain);
+#pragma omp parallel for schedule(static) if (nblk > 1)
+  for (long b = 0; b < nblk; ++b) {
+    const size_t o = size_t(b) * grain;
+    memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+           std::min(grain, bytes - o));
+  }
+}
+
 // upload rows of host records (reference layout) into planes; returns the
 // summed block partials {mass0, mass1, weighted sumsq}
 static void host_to_planes(otfx_engine* e, const double* h0, const double* h1, const PackMap& m,
                            void* planes, double sums[3]) {
+  PinnedPool& P = pinned_pool();
+  std::lock_guard<std::mutex> lock(P.mu);
   const int n = e->d.n;
   const size_t row_bytes = size_t(n) * m.rec * sizeof(double);
-  const int inputs = h1 ? 2 : 1;
-  int chunk = int(std::max<size_t>(1, e->stage_bytes / (inputs * row_bytes)));
+  const size_t slot = std::min(PinnedPool::kSlot, e->stage_bytes / 4);
+  int chunk = int(std::max<size_t>(1, slot / row_bytes));
   chunk = std::min(chunk, e->rows);
-  require(size_t(chunk) * row_bytes * inputs <= e->stage_bytes, OTFX_EUNSUPPORTED,
+  require(size_t(chunk) * row_bytes <= slot, OTFX_EUNSUPPORTED,
           "grid row too large for the staging buffer");
-  sums[0] = sums[1] = sums[2] = 0.0;
-  double* st0 = e->d_stage;
-  double* st1 = e->d_stage + size_t(chunk) * n * m.rec;
-  for (int r0 = 0; r0 < e->rows; r0 += chunk) {
+  const int nchunks = (e->rows + chunk - 1) / chunk;
+  std::vector<double> part(size_t(nchunks) * kPackBlocks * 3);
+  double* hp;
+  CK(cudaMallocHost(&hp, part.size() * sizeof(double)));
+  for (int k = 0; k < nchunks; ++k) {
+    const int b = k & 1;
+    const int r0 = k * chunk;
     const int nr = std::min(chunk, e->rows - r0);
     const size_t off = size_t(r0) * n * m.rec;
     const size_t bytes = size_t(nr) * row_bytes;
-    CK(cudaMemcpyAsync(st0, h0 + off, bytes, cudaMemcpyHostToDevice, e->stream));
-    if (h1) CK(cudaMemcpyAsync(st1, h1 + off, bytes, cudaMemcpyHostToDevice, e->stream));
+    unsigned char* pin0 = P.buf + size_t(2 * b) * PinnedPool::kSlot;
+    unsigned char* pin1 = pin0 + PinnedPool::kSlot;
+    double* st0 = e->d_stage + size_t(b) * (e->stage_bytes / 2 / sizeof(double));
+    double* st1 = st0 + slot / sizeof(double);
+    if (k >= 2) CK(cudaEventSynchronize(P.ev[b]));  // slot b free again
+    par_copy(pin0, h0 + off, bytes);
+    if (h1) par_copy(pin1, h1 + off, bytes);
+    CK(cudaMemcpyAsync(st0, pin0, bytes, cudaMemcpyHostToDevice, e->stream));
+    if (h1) CK(cudaMemcpyAsync(st1, pin1, bytes, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaEventRecord(P.ev[b], e->stream));
     if (e->elem == 8) pack_chunk<double>(e, st0, h1 ? st1 : nullptr, int64_t(nr) * n, planes, 1 + r0, m);
     else pack_chunk<float>(e, st0, h1 ? st1 : nullptr, int64_t(nr) * n, planes, 1 + r0, m);
-    CK(cudaMemcpyAsync(e->h_pack_part, e->d_pack_part, kPackBlocks * 3 * sizeof(double),
-                       cudaMemcpyDeviceToHost, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
-    for (int b = 0; b < kPackBlocks; ++b)
-      for (int q = 0; q < 3; ++q) sums[q] += e->h_pack_part[b * 3 + q];
+    CK(cudaMemcpyAsync(hp + size_t(k) * kPackBlocks * 3, e->d_pack_part,
+                       kPackBlocks * 3 * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
   }
+  CK(cudaStreamSynchronize(e->stream));
+  sums[0] = sums[1] = sums[2] = 0.0;
+  for (size_t q = 0; q < part.size(); q += 3) {
+    sums[0] += hp[q];
+    sums[1] += hp[q + 1];
+    sums[2] += hp[q + 2];
+  }
+  cudaFreeHost(hp);
 }
 
 static void planes_to_host(otfx_engine* e, const void* planes, const UnpackMap& m, double* h) {
+  PinnedPool& P = pinned_pool();
+  std::lock_guard<std::mutex> lock(P.mu);
   const int n = e->d.n;
   const size_t row_bytes = size_t(n) * m.rec * sizeof(double);
-  int chunk = int(std::max<size_t>(1, e->stage_bytes / row_bytes));
+  const size_t slot = std::min(PinnedPool::kSlot, e->stage_bytes / 4);
+  int chunk = int(std::max<size_t>(1, slot / row_bytes));
   chunk = std::min(chunk, e->rows);
-  for (int r0 = 0; r0 < e->rows; r0 += chunk) {
+  require(size_t(chunk) * row_bytes <= slot, OTFX_EUNSUPPORTED,
+          "grid row too large for the staging buffer");
+  const int nchunks = (e->rows + chunk - 1) / chunk;
+  auto launch = [&](int k) {
+    const int b = k & 1;
+    const int r0 = k * chunk;
     const int nr = std::min(chunk, e->rows - r0);
     const int64_t ncell = int64_t(nr) * n;
+    double* st = e->d_stage + size_t(b) * (e->stage_bytes / 2 / sizeof(double));
+    unsigned char* pin = P.buf + size_t(2 * b) * PinnedPool::kSlot;
     if (e->elem == 8)
       unpack_kernel<double><<<kPackBlocks, 256, 0, e->stream>>>(
-          static_cast<const double*>(planes), e->plane, e->pitch, 1 + r0, ncell, n, m, e->d_stage);
+          static_cast<const double*>(planes), e->plane, e->pitch, 1 + r0, ncell, n, m, st);
     else
       unpack_kernel<float><<<kPackBlocks, 256, 0, e->stream>>>(
-          static_cast<const float*>(planes), e->plane, e->pitch, 1 + r0, ncell, n, m, e->d_stage);
+          static_cast<const float*>(planes), e->plane, e->pitch, 1 + r0, ncell, n, m, st);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(h + size_t(r0) * n * m.rec, e->d_stage, size_t(nr) * row_bytes,
-                       cudaMemcpyDeviceToHost, e->stream));
-    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaMemcpyAsync(pin, st, size_t(nr) * row_bytes, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaEventRecord(P.ev[b], e->stream));
+  };
+  launch(0);
+  for (int k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks) launch(k + 1);  // next chunk's DMA overlaps this chunk's memcpy
+    const int b = k & 1;
+    CK(cudaEventSynchronize(P.ev[b]));
+    const int r0 = k * chunk;
+    const int nr = std::min(chunk, e->rows - r0);
+    par_copy(h + size_t(r0) * n * m.rec, P.buf + size_t(2 * b) * PinnedPool::kSlot,
+             size_t(nr) * row_bytes);
   }
 }
 
@@ -823,10 +899,6 @@ static void drop_graphs(otfx_engine* e) {
   e->graphs.clear();
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
 
 static void create(const otfx_engine_desc* d, otfx_engine* e) {
   require(d != nullptr, OTFX_EINVAL, "null descriptor");
@@ -935,7 +1007,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
 
   // staging: up to 64 MB, at least two grid rows of the widest record
   const int max_rec = std::max(2 * e->K * e->K * std::max(1, d->ell) * 2, 16);
-  e->stage_bytes = std::max<size_t>(size_t(64) << 20, size_t(2) * n * max_rec * sizeof(double));
+  e->stage_bytes = std::max<size_t>(size_t(128) << 20, size_t(4) * n * max_rec * sizeof(double));
 
   const size_t n_sweep = size_t(e->gx) * e->gy * 4, n_pe = size_t(e->ex) * e->ey * 8,
                n_me = size_t(e->ex) * e->ey * 2;

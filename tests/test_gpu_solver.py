@@ -266,3 +266,36 @@ def test_local_slabs_bit_identical(P, n):
     np.testing.assert_allclose(out, ref, rtol=1e-12)
     for e in reversed(slabs):  # slab 0 owns the shared stream
         e.close()
+
+
+# ---------------------------------------------------------------------------
+# both sweep implementations (TMA-streamed default, register-streamed
+# fallback) produce the same bits
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_tma_and_register_sweeps_identical(monkeypatch, precision):
+    l0, l1 = synthetic.rgb_disk_pair(300)
+    gph = pk.triangle_graph((1.0, 1.2, 0.9))
+    cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", alpha=0.05, tol_gap=1e-300,
+                          tol_feas=1e-300, max_iters=120, check_every=40)
+    outs = []
+    for tma in ("1", "0"):
+        monkeypatch.setenv("OTFX_TMA", tma)
+        eng = build_engine("vector", 300, cfg, graph=gph, precision=precision)
+        assert (eng.info()["tma_stages"] > 0) == (tma == "1")
+        eng.set_marginals(l0, l1)
+        hist, it, conv, wall = eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+        outs.append((g.hist_array(pk.SolveReport(conv, it, 0.0, hist)), eng.get_state()))
+        eng.close()
+    (h1, s1), (h2, s2) = outs
+    np.testing.assert_array_equal(h1, h2)
+    for a, b in zip(s1, s2):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_default_path_is_tma_streamed():
+    cfg = pk.SolverConfig()
+    eng = build_engine("vector", 1024, cfg, graph=pk.triangle_graph())
+    inf = eng.info()
+    eng.close()
+    assert inf["tma_stages"] >= 3 and inf["tile_cols"] == 124
