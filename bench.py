@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-secondary", action="store_true",
+                   help="skip the BASELINE configs[0..3] side measurements")
     return p.parse_args()
 
 
@@ -286,6 +288,9 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.ref_n, args.cpu_seconds)
+    secondary = None
+    if rank == 0 and world == 1 and not args.no_secondary:
+        secondary = secondary_configs(args, local)
     if rank == 0:
         state_gb = info["state_bytes"] * 2 / 1e9
         line = {
@@ -314,6 +319,7 @@ def run_ours(args):
                          "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "secondary": secondary,
             "gpu_launches": args.steps * (ips - 1 + 3),
             "clocks": clk.summary(),
         }
@@ -321,6 +327,80 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def secondary_configs(args, device):
+    """BASELINE configs[0..3] (the parity configurations) timed on the GPU
+    through the engine (device time, CUDA events) next to the NumPy port of the
+    reference on a bounded CPU sample.  Reported beside the headline, not as it."""
+    import torch
+    from threadpoolctl import threadpool_limits
+
+    import paper_1712_10279_b200 as pk
+    from oracle.pdhg import OracleEngine
+    from paper_1712_10279_b200 import synthetic
+    from paper_1712_10279_b200.solver import build_engine
+
+    tri = pk.triangle_graph()
+    cases = [
+        ("C1 vector 3ch 64^2 x2000 (exact count)", "vector", 64,
+         lambda: synthetic.rgb_disk_pair(64), tri, None,
+         pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1"), 2000, 2000, 200),
+        ("C2 vector 3ch 256^2 to convergence (tau=6; the reference does not converge "
+         "within max_iters=200000)", "vector", 256, lambda: synthetic.rgb_disk_pair(256), tri, None,
+         pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1"), 200_000, 200_000, 20),
+        ("C3 matrix 2x2 Hermitian 128^2 l1nuc/l1nuc x300", "matrix", 128,
+         lambda: synthetic.blob_pair_k2(128), None, pk.lindblad_pair_k2(),
+         pk.SolverConfig(tau=30.0, norm_u="l1nuc", norm_w="l1nuc"), 300, 300, 5),
+        ("C4 matrix 3x3 DTI 256^2 l2/l1 x500", "matrix", 256,
+         lambda: synthetic.matrix_blob_fixtures(256)[:2], None, pk.default_lindblad3(),
+         pk.SolverConfig(tau=30.0, norm_u="l2", norm_w="l1"), 500, 500, 10),
+    ]
+    out = []
+    for name, kind, n, gen, graph, lind, cfg0, iters, max_iters, cpu_iters in cases:
+        l0, l1 = gen()
+        tol = dict(tol_gap=cfg0.tol_gap, tol_feas=cfg0.tol_feas) if "convergence" in name else \
+            dict(tol_gap=1e-300, tol_feas=1e-300)
+        cfg = pk.SolverConfig(tau=cfg0.tau, norm_u=cfg0.norm_u, norm_w=cfg0.norm_w, alpha=1.0,
+                              max_iters=max_iters, check_every=100, **tol)
+        complex_path = kind == "matrix" and (cfg.norm_u.value == "l1nuc" or np.any(np.imag(l0)))
+        stream = torch.cuda.Stream()
+        eng = build_engine(kind, n, cfg, graph=graph, lindblad=lind, complex_path=complex_path,
+                           device=device, stream=stream.cuda_stream)
+        eng.set_marginals(l0, l1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        hist, it, conv, wall = eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+        b.record(stream)
+        torch.cuda.synchronize()
+        gms = a.elapsed_time(b)
+        eng.close()
+        # CPU: the NumPy port of the reference engine on a bounded sample
+        if kind == "vector":
+            ref = OracleEngine("vector", l0 - l1, n, cfg.tau, norm_u=cfg.norm_u.value,
+                               norm_w=cfg.norm_w.value, chan=graph.coefficients(),
+                               lam_chan=pk.lambda_max_graph(graph))
+        else:
+            mats = lind.matrices
+            diff = l0 - l1
+            dt = np.complex128 if complex_path else np.float64
+            ref = OracleEngine("matrix", diff if complex_path else np.ascontiguousarray(diff.real),
+                               n, cfg.tau, norm_u=cfg.norm_u.value, norm_w=cfg.norm_w.value,
+                               chan=mats if complex_path else np.ascontiguousarray(np.real(mats)),
+                               lam_chan=pk.lambda_max_L(lind), dtype=dt)
+        with threadpool_limits(limits=os.cpu_count() or 1):
+            ref.step()
+            t0 = time.perf_counter()
+            for _ in range(cpu_iters):
+                ref.step()
+            cs = time.perf_counter() - t0
+        gpu_rate = n * n * it / (gms * 1e-3)
+        cpu_rate = n * n * cpu_iters / cs
+        out.append(dict(config=name, n=n, iterations=it, converged=conv,
+                        final_primal=hist[-1].primal, gpu_seconds=gms * 1e-3,
+                        gpu_cell_updates_per_s=gpu_rate, cpu_cell_updates_per_s=cpu_rate,
+                        cpu_sample_iterations=cpu_iters, speedup=gpu_rate / cpu_rate))
+    return out
 
 
 def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn):
