@@ -385,8 +385,10 @@ static bool plan_stages(otfx_engine* e, int S) {
   L.S = S;
   const int row = L.tw * e->elem;
   const int bu = 2 * e->NP * row, bw = e->NWact * row, bd = e->NP * row, bp = e->NP * row;
+  // same layout as StageShape<P,T> (w sub-block sized for the policy capacity)
+  const int nwcap = e->has_w ? e->LMAX * e->NWS : 1;
   L.off_w = round_up(bu, 128);
-  L.off_d = L.off_w + round_up(bw, 128);
+  L.off_d = L.off_w + round_up(nwcap * row, 128);
   L.off_p = L.off_d + round_up(bd, 128);
   L.stage_bytes = L.off_p + round_up(bp, 128);
   L.bytes_full = bu + bw + bd + bp;

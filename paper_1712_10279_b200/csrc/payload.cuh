@@ -22,11 +22,13 @@ namespace otfx {
 
 template <typename T>
 __device__ __forceinline__ T soft_factor(T r, T thr) {
-  // S/shrink.py:120-136: r = max(r, tiny); r = thr / r; r = 1 - r; r = max(r, 0)
-  r = maxT(r, tiny_of<T>());
-  r = thr / r;
-  r = T(1) - r;
-  return maxT(r, T(0));
+  // S/shrink.py:120-136: r = max(r, tiny); r = thr / r; r = 1 - r; r = max(r, 0).
+  // For r <= thr the reference's value is exactly 0 (thr/r >= 1 rounds to >= 1,
+  // and thr/tiny or the fp32 thr/0 = inf give 0 too), so the division only runs
+  // where it matters; for r > thr, 1 - thr/r >= 0 and the max is a no-op.
+  // Bit-identical to the reference's sequence, without fp32 div-by-zero slow paths.
+  const T q = thr / (r > thr ? r : T(1));
+  return r > thr ? T(1) - q : T(0);
 }
 
 template <typename T>
@@ -50,7 +52,8 @@ struct VecPolicy {
   __device__ static __forceinline__ double ww(int) { return 1.0; }
 
   // u payload x[dir][c]; prox of mu*||.|| then the eps scaling (S/shrink.py:208-240)
-  __device__ static void prox_u(T (&x)[2][NP], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void prox_u(T (&x)[2][NP], const PA& A) {
     const T thr = A.mu;
     if (A.norm_u == NORM_L2) {
       T s = T(0);
@@ -85,7 +88,8 @@ struct VecPolicy {
   }
 
   // graph gradient diag(1/c) D^T phi  (S/graph.py:105-114)
-  __device__ static void grad_c(const T (&p)[NP], T (&g)[NWA], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void grad_c(const T (&p)[NP], T (&g)[NWA], const PA& A) {
 #pragma unroll
     for (int e = 0; e < NWA; ++e) {
       T s = T(0);
@@ -96,7 +100,8 @@ struct VecPolicy {
   }
 
   // graph divergence -D diag(1/c) y  (S/graph.py:117-123)
-  __device__ static void div_c(const T (&y)[NWA], T (&d)[NP], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void div_c(const T (&y)[NWA], T (&d)[NP], const PA& A) {
 #pragma unroll
     for (int c = 0; c < K; ++c) {
       T s = T(0);
@@ -106,7 +111,8 @@ struct VecPolicy {
     }
   }
 
-  __device__ static void prox_w(T (&x)[NWA], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void prox_w(T (&x)[NWA], const PA& A) {
     const T thr = A.thr_w;
     if (A.norm_w == NORM_L2) {
       T s = T(0);
@@ -465,7 +471,8 @@ struct SymPolicy {
     return s + (o + o);
   }
 
-  __device__ static void prox_u(T (&x)[2][NP], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void prox_u(T (&x)[2][NP], const PA& A) {
     const T thr = A.mu;
     if (A.norm_u == NORM_L2) {
       const T f = soft_factor(sqrt(ssq_p(x[0]) + ssq_p(x[1])), thr);
@@ -494,12 +501,14 @@ struct SymPolicy {
     }
   }
 
-  __device__ static __forceinline__ T L(const SweepArgs<T>& A, int s, int a, int b) {
+  template <class PA>
+  __device__ static __forceinline__ T L(const PA& A, int s, int a, int b) {
     return T(A.coef[((s * K + a) * K + b) * 2]);
   }
 
   // [L_s, X] = P - P^T with P = L_s X  (S/lindblad.py:87-107)
-  __device__ static void grad_c(const T (&p)[NP], T (&g)[NWA], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void grad_c(const T (&p)[NP], T (&g)[NWA], const PA& A) {
     T X[K][K];
     unpack(p, X);
 #pragma unroll
@@ -522,7 +531,8 @@ struct SymPolicy {
   }
 
   // sum_s Z_s L_s + (.)^T  (S/lindblad.py:110-129)
-  __device__ static void div_c(const T (&y)[NWA], T (&d)[NP], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void div_c(const T (&y)[NWA], T (&d)[NP], const PA& A) {
     T Tm[K][K];
 #pragma unroll
     for (int a = 0; a < K; ++a)
@@ -558,7 +568,8 @@ struct SymPolicy {
       for (int b = a + 1; b < K; ++b) d[K + pair_index<K>(a, b)] = Tm[a][b] + Tm[b][a];
   }
 
-  __device__ static void prox_w(T (&x)[NWA], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void prox_w(T (&x)[NWA], const PA& A) {
     const T thr = A.thr_w;
     if (A.norm_w == NORM_L2) {
       T s = T(0);
@@ -749,7 +760,8 @@ struct HermPolicy {
     (void)len;
   }
 
-  __device__ static void prox_u(T (&x)[2][NP], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void prox_u(T (&x)[2][NP], const PA& A) {
     const T thr = A.mu;
     if (A.norm_u == NORM_L2) {
       const T f = soft_factor(sqrt(ssq_p(x[0]) + ssq_p(x[1])), thr);
@@ -784,13 +796,15 @@ struct HermPolicy {
     }
   }
 
-  __device__ static __forceinline__ cpx<T> L(const SweepArgs<T>& A, int s, int a, int b) {
+  template <class PA>
+  __device__ static __forceinline__ cpx<T> L(const PA& A, int s, int a, int b) {
     const int o = ((s * K + a) * K + b) * 2;
     return {T(A.coef[o]), T(A.coef[o + 1])};
   }
 
   // [L_s, X] = P - P^H, P = L_s X
-  __device__ static void grad_c(const T (&p)[NP], T (&g)[NWA], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void grad_c(const T (&p)[NP], T (&g)[NWA], const PA& A) {
     T xr[K][K], xi[K][K];
     unpack_h(p, xr, xi);
 #pragma unroll
@@ -820,7 +834,8 @@ struct HermPolicy {
   }
 
   // T + T^H, T = sum_s Z_s L_s
-  __device__ static void div_c(const T (&y)[NWA], T (&d)[NP], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void div_c(const T (&y)[NWA], T (&d)[NP], const PA& A) {
     cpx<T> Tm[K][K];
 #pragma unroll
     for (int a = 0; a < K; ++a)
@@ -862,7 +877,8 @@ struct HermPolicy {
       }
   }
 
-  __device__ static void prox_w(T (&x)[NWA], const SweepArgs<T>& A) {
+  template <class PA>
+  __device__ static void prox_w(T (&x)[NWA], const PA& A) {
     const T thr = A.thr_w;
     if (A.norm_w == NORM_L2) {
       T s = T(0);

@@ -33,10 +33,11 @@ template <class P, typename T>
 struct Cell {
   static constexpr int NP = P::NP;
   // u' for one cell from phi(i,j), phi(i+1,j), phi(i,j+1) and u(i,j)
+  template <class PA>
   __device__ static __forceinline__ void flux(const T (&ph)[NP], const T (&phx)[NP],
                                               const T (&phy)[NP], bool hasx, bool hasy,
                                               const T (&uo)[2][NP], T (&un)[2][NP],
-                                              const SweepArgs<T>& A) {
+                                              const PA& A) {
 #pragma unroll
     for (int c = 0; c < NP; ++c) {
       const T gx = hasx ? (phx[c] - ph[c]) * A.inv_dx : T(0);

@@ -53,27 +53,80 @@ struct TmaSweepArgs {
   StageLayout L;
 };
 
+// Channel coefficients as the kernels read them: the small vector D/c matrix
+// is pulled into registers once per CTA; the Lindblad stacks stay in the
+// (constant-cached) parameter space.
+template <class P, typename T, bool REG = (P::NWS == 1)>
+struct CoefView;
+template <class P, typename T>
+struct CoefView<P, T, true> {
+  T c[P::K * P::LMAX];
+  __device__ __forceinline__ void load(const SweepArgs<T>& A) {
+#pragma unroll
+    for (int q = 0; q < P::K * P::LMAX; ++q) c[q] = T(A.coef[q]);
+  }
+  __device__ __forceinline__ T operator[](int q) const { return c[q]; }
+};
+template <class P, typename T>
+struct CoefView<P, T, false> {
+  const double* c;
+  __device__ __forceinline__ void load(const SweepArgs<T>& A) { c = A.coef; }
+  __device__ __forceinline__ double operator[](int q) const { return c[q]; }
+};
+
+// The scalars the per-cell math reads, held in registers for the whole CTA
+// (the policies are duck-typed on these field names).
+template <class P, typename T>
+struct HotArgs {
+  T mu, thr_w, nu, tau, inv_dx, den_u, den_w;
+  int has_eps, norm_u, norm_w, ell;
+  double alpha;
+  CoefView<P, T> coef;
+  __device__ __forceinline__ void load(const SweepArgs<T>& A) {
+    mu = A.mu; thr_w = A.thr_w; nu = A.nu; tau = A.tau; inv_dx = A.inv_dx;
+    den_u = A.den_u; den_w = A.den_w; has_eps = A.has_eps;
+    norm_u = A.norm_u; norm_w = A.norm_w; ell = A.ell; alpha = A.alpha;
+    coef.load(A);
+  }
+};
+
+// compile-time shared-memory layout of one TMA row stage
+template <class P, typename T>
+struct StageShape {
+  static constexpr int H = 16 / int(sizeof(T));     // halo columns (16 B)
+  static constexpr int TILE = 124;                  // output columns per CTA
+  static constexpr int TW = TILE + 2 * H;           // staged columns
+  static constexpr int ROW = TW * int(sizeof(T));
+  static constexpr int R128(int x) { return (x + 127) / 128 * 128; }
+  static constexpr int OFF_W = R128(2 * P::NP * ROW);
+  static constexpr int OFF_D = OFF_W + R128((P::NWA > 0 ? P::NWA : 1) * ROW);
+  static constexpr int OFF_P = OFF_D + R128(P::NP * ROW);
+  static constexpr int BYTES = OFF_P + R128(P::NP * ROW);
+};
+
 template <class P, typename T, bool CHECK>
 __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ TmaSweepArgs<T> G,
                                                        const __grid_constant__ TmaSet M) {
+  using SS = StageShape<P, T>;
   constexpr int NP = P::NP;
   constexpr int NWA = P::NWA;
+  constexpr int TW = SS::TW;
   const SweepArgs<T>& A = G.s;
   const StageLayout& L = G.L;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [S]
   uint64_t* empty = full + 8;                          // [S]
+  unsigned char* stages = smem + 128;
   double* sred = reinterpret_cast<double*>(smem + L.off_red);
 
   const int CW = L.cw;
-  const int TW = L.tw;
   const int S = L.S;
   const int t = threadIdx.x;
   const int warp = t >> 5, lane = t & 31;
   const bool producer = warp >= CW;
-  const int c0 = blockIdx.x * L.tile;
-  const int sc = L.h + 31 * warp + lane - 1;  // staged column index of this thread's column
-  const int j = c0 - L.h + sc;                // = c0 + 31 warp + lane - 1
+  const int c0 = blockIdx.x * SS::TILE;
+  const int sc = SS::H + 31 * warp + lane - 1;  // staged column index of this thread's column
+  const int j = c0 - SS::H + sc;                // = c0 + 31 warp + lane - 1
   const int n = A.n;
   const bool out = !producer && lane > 0 && j < n;  // lane 0 is the overlap column
   const bool hasy = j + 1 < n;
@@ -81,24 +134,6 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
   const int gr1 = min(gr0 + A.rows_per_block, A.row_end);
   const int qbase = gr0 - 1;
   const int qmax = gr1 - qbase;  // index of the phi-only tail stage
-  const int64_t pl = A.plane;
-  const int nwp = A.ell * P::NWS;
-
-  auto stage = [&](int q) -> unsigned char* {
-    return smem + L.off_stages + (q % S) * L.stage_bytes;
-  };
-  auto U = [&](int q, int p, int col) -> T {
-    return reinterpret_cast<const T*>(stage(q))[p * TW + col];
-  };
-  auto Wv = [&](int q, int p, int col) -> T {
-    return reinterpret_cast<const T*>(stage(q) + L.off_w)[p * TW + col];
-  };
-  auto Dv = [&](int q, int p, int col) -> T {
-    return reinterpret_cast<const T*>(stage(q) + L.off_d)[p * TW + col];
-  };
-  auto PH = [&](int q, int p, int col) -> T {
-    return reinterpret_cast<const T*>(stage(q) + L.off_p)[p * TW + col];
-  };
 
   if (t == 0) {
     for (int s = 0; s < S; ++s) {
@@ -113,43 +148,61 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
   if (producer) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      const int cx = c0 - L.h;
+      const int cx = c0 - SS::H;
+      int slot = 0, use = 0;
       for (int q = 0; q <= qmax; ++q) {
-        const int slot = q % S;
-        if (q >= S) mbar_wait(&empty[slot], ((q / S) - 1) & 1);
+        if (q >= S) mbar_wait(&empty[slot], (use - 1) & 1);
         uint64_t* bar = &full[slot];
         const int r = qbase + q;
         const int lrow = r - A.row_begin + 1;
-        unsigned char* st = stage(q);
+        unsigned char* st = stages + slot * SS::BYTES;
         if (q == 0 || q == qmax) {
           const bool load = (q == 0) ? (gr0 > 0) : (r < n);
           if (!load) {
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-            continue;
-          }
-          if (q == 0) {
-            mbar_expect_tx(bar, L.bytes_flux);
-            tma_load_3d(st, &M.u, bar, cx, lrow, 0);
           } else {
-            mbar_expect_tx(bar, L.bytes_phi);
+            if (q == 0) {
+              mbar_expect_tx(bar, L.bytes_flux);
+              tma_load_3d(st, &M.u, bar, cx, lrow, 0);
+            } else {
+              mbar_expect_tx(bar, L.bytes_phi);
+            }
+            tma_load_3d(st + SS::OFF_P, &M.phi, bar, cx, lrow, 0);
           }
-          tma_load_3d(st + L.off_p, &M.phi, bar, cx, lrow, 0);
         } else {
           mbar_expect_tx(bar, L.bytes_full);
           tma_load_3d(st, &M.u, bar, cx, lrow, 0);
-          if (P::HAS_W) tma_load_3d(st + L.off_w, &M.w, bar, cx, lrow, 0);
-          tma_load_3d(st + L.off_d, &M.diff, bar, cx, lrow, 0);
-          tma_load_3d(st + L.off_p, &M.phi, bar, cx, lrow, 0);
+          if (P::HAS_W) tma_load_3d(st + SS::OFF_W, &M.w, bar, cx, lrow, 0);
+          tma_load_3d(st + SS::OFF_D, &M.diff, bar, cx, lrow, 0);
+          tma_load_3d(st + SS::OFF_P, &M.phi, bar, cx, lrow, 0);
+        }
+        if (++slot == S) {
+          slot = 0;
+          ++use;
         }
       }
     }
   } else {
     // ------------------------------------------------------------ consumers
-    auto wait_full = [&](int q) { mbar_wait(&full[q % S], (q / S) & 1); };
-    auto release = [&](int q) {
+    HotArgs<P, T> H;
+    H.load(A);
+    const int nwp = H.ell * P::NWS;
+    const int64_t pl = A.plane;
+    // ring cursor for stage q (slot, phase parity) and stage q+1
+    int s0 = 0, ph0 = 0;
+    auto adv = [&](int& s, int& ph) {
+      if (++s == S) {
+        s = 0;
+        ph ^= 1;
+      }
+    };
+    auto base = [&](int s) -> const T* {
+      return reinterpret_cast<const T*>(stages + s * SS::BYTES) + sc;
+    };
+    auto release = [&](int s) {
       __syncwarp();
       if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[q % S]))
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
                      : "memory");
     };
     T uxb_prev[NP], dux_prev[NP];
@@ -158,45 +211,63 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
       uxb_prev[c] = T(0);
       dux_prev[c] = T(0);
     }
+    int s1 = 1, ph1 = 0;  // cursor of stage q+1
+    if (S == 1) s1 = 0;
     // halo row gr0-1: ubar_x(gr0-1, j) from the read-only iterate
-    wait_full(0);
+    mbar_wait(&full[s0], ph0);
     if (gr0 > 0) {
-      wait_full(1);
+      mbar_wait(&full[s1], ph1);
+      const T* b0 = base(s0);
+      const T* b1 = base(s1);
       T pm[NP], px[NP], py[NP], uo[2][NP], un[2][NP];
 #pragma unroll
       for (int c = 0; c < NP; ++c) {
-        pm[c] = PH(0, c, sc);
-        py[c] = PH(0, c, sc + 1);
-        px[c] = PH(1, c, sc);
-        uo[0][c] = U(0, c, sc);
-        uo[1][c] = U(0, NP + c, sc);
+        const T* pp = reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(b0) + SS::OFF_P);
+        pm[c] = pp[c * TW];
+        py[c] = pp[c * TW + 1];
+        px[c] = reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(b1) + SS::OFF_P)[c * TW];
+        uo[0][c] = b0[c * TW];
+        uo[1][c] = b0[(NP + c) * TW];
       }
-      Cell<P, T>::flux(pm, px, py, true, hasy, uo, un, A);
+      Cell<P, T>::flux(pm, px, py, true, hasy, uo, un, H);
 #pragma unroll
       for (int c = 0; c < NP; ++c) {
         uxb_prev[c] = (un[0][c] + un[0][c]) - uo[0][c];
         dux_prev[c] = un[0][c] - uo[0][c];
       }
     }
-    release(0);
+    release(s0);
+    adv(s0, ph0);  // stage 0 -> stage 1 becomes "q"
+    s1 = s0;
+    ph1 = ph0;
+    adv(s1, ph1);
 
+    T* gu = A.b.u;
+    T* gphi = A.b.phi;
+    T* gw = A.b.w;
     for (int i = gr0; i < gr1; ++i) {
-      const int q = i - qbase;
       const bool hasx = i + 1 < n;
-      wait_full(q);
-      wait_full(q + 1);
+      mbar_wait(&full[s0], ph0);
+      mbar_wait(&full[s1], ph1);
+      const unsigned char* st0 = reinterpret_cast<const unsigned char*>(base(s0));
+      const unsigned char* st1 = reinterpret_cast<const unsigned char*>(base(s1));
+      const T* sU = reinterpret_cast<const T*>(st0);
+      const T* sW = reinterpret_cast<const T*>(st0 + SS::OFF_W);
+      const T* sD = reinterpret_cast<const T*>(st0 + SS::OFF_D);
+      const T* sP = reinterpret_cast<const T*>(st0 + SS::OFF_P);
+      const T* sPn = reinterpret_cast<const T*>(st1 + SS::OFF_P);
       T phc[NP], un[2][NP], ub[2][NP], uo[2][NP], lub[NP], ldu[NP];
       {
         T phx[NP], phy[NP];
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
-          phc[c] = PH(q, c, sc);
-          phy[c] = PH(q, c, sc + 1);
-          phx[c] = PH(q + 1, c, sc);
-          uo[0][c] = U(q, c, sc);
-          uo[1][c] = U(q, NP + c, sc);
+          phc[c] = sP[c * TW];
+          phy[c] = sP[c * TW + 1];
+          phx[c] = sPn[c * TW];
+          uo[0][c] = sU[c * TW];
+          uo[1][c] = sU[(NP + c) * TW];
         }
-        Cell<P, T>::flux(phc, phx, phy, hasx, hasy, uo, un, A);
+        Cell<P, T>::flux(phc, phx, phy, hasx, hasy, uo, un, H);
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
           ub[0][c] = (un[0][c] + un[0][c]) - uo[0][c];
@@ -208,12 +279,12 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
       }
       T df[NP], wo[NWA];
 #pragma unroll
-      for (int c = 0; c < NP; ++c) df[c] = Dv(q, c, sc);
+      for (int c = 0; c < NP; ++c) df[c] = sD[c * TW];
       if (P::HAS_W) {
 #pragma unroll
-        for (int e = 0; e < NWA; ++e) wo[e] = e < nwp ? Wv(q, e, sc) : T(0);
+        for (int e = 0; e < NWA; ++e) wo[e] = e < nwp ? sW[e * TW] : T(0);
       }
-      release(q);  // stage q fully consumed (stage q+1 stays for the next row)
+      release(s0);  // stage q fully consumed (stage q+1 stays for the next row)
       if (out) {
         const int64_t o = cell_off(A, i, j);
         T rhs[NP];
@@ -223,42 +294,45 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
           if (i > 0) d = d - uxb_prev[c];
           d = d + ub[1][c];
           if (j > 0) d = d - lub[c];
-          d = d * A.inv_dx;
+          d = d * H.inv_dx;
           rhs[c] = d - df[c];
         }
         T wn[NWA], dwv[NWA];
         if (P::HAS_W) {
-          T g[NWA];
-          P::grad_c(phc, g, A);
+          T gc[NWA];
+          P::grad_c(phc, gc, H);
 #pragma unroll
-          for (int e = 0; e < NWA; ++e) wn[e] = g[e] * A.nu + wo[e];
-          P::prox_w(wn, A);
+          for (int e = 0; e < NWA; ++e) wn[e] = gc[e] * H.nu + wo[e];
+          P::prox_w(wn, H);
           T wb[NWA], dv[NP];
 #pragma unroll
           for (int e = 0; e < NWA; ++e) {
             wb[e] = (wn[e] + wn[e]) - wo[e];
             dwv[e] = wn[e] - wo[e];
           }
-          P::div_c(wb, dv, A);
+          P::div_c(wb, dv, H);
 #pragma unroll
           for (int c = 0; c < NP; ++c) rhs[c] = rhs[c] + dv[c];
         }
         T phnew[NP];
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
-          rhs[c] = rhs[c] * A.tau;
+          rhs[c] = rhs[c] * H.tau;
           phnew[c] = phc[c] + rhs[c];
         }
+        T* pu = gu + o;
+        T* pp = gphi + o;
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
-          A.b.u[c * pl + o] = un[0][c];
-          A.b.u[(NP + c) * pl + o] = un[1][c];
-          A.b.phi[c * pl + o] = phnew[c];
+          pu[c * pl] = un[0][c];
+          pu[(NP + c) * pl] = un[1][c];
+          pp[c * pl] = phnew[c];
         }
         if (P::HAS_W) {
+          T* pw = gw + o;
 #pragma unroll
           for (int e = 0; e < NWA; ++e)
-            if (e < nwp) A.b.w[e * pl + o] = wn[e];
+            if (e < nwp) pw[e * pl] = wn[e];
         }
         if (CHECK) {
           T cross[NP];
@@ -271,11 +345,11 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
             if (i > 0) d = d - dux_prev[c];
             d = d + dy;
             if (j > 0) d = d - ldu[c];
-            cross[c] = d * A.inv_dx;
+            cross[c] = d * H.inv_dx;
           }
           if (P::HAS_W) {
             T dv[NP];
-            P::div_c(dwv, dv, A);
+            P::div_c(dwv, dv, H);
 #pragma unroll
             for (int c = 0; c < NP; ++c) cross[c] = cross[c] + dv[c];
 #pragma unroll
@@ -294,6 +368,9 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
         uxb_prev[c] = ub[0][c];
         if (CHECK) dux_prev[c] = un[0][c] - uo[0][c];
       }
+      s0 = s1;
+      ph0 = ph1;
+      adv(s1, ph1);
     }
   }
 
