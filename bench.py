@@ -235,32 +235,26 @@ def run_ours(args):
     m0, m1 = eng.set_marginals(l0, l1)
     info = eng.info()
 
-    def one_step(ev=None):
-        if ev is not None:
-            ev[0].record(stream)
-        eng.step(ips - 1)
-        if ev is not None:
-            ev[1].record(stream)
-        return eng.step_check()
-
-    for _ in range(args.warmup):
-        one_step()
+    # warm-up: W check periods through the run loop (graph capture, clocks)
+    eng.run(1e-300, 1e-300, args.warmup * ips, ips)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eng.timing(1)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         start.record(stream)
-        last = None
-        for q in range(args.steps):
-            last = one_step(evs[q])
+        # K check periods = K*ips iterations of the reference run loop
+        # (S/solver.py:303-315), checks included, on the device
+        hist, it_done, _, _ = eng.run(1e-300, 1e-300, args.steps * ips, ips)
         stop.record(stream)
         torch.cuda.synchronize()
+    assert it_done == args.steps * ips
+    last = (hist[-1].primal, hist[-1].dual, hist[-1].gap_ratio)
     ms = start.elapsed_time(stop)
-    sweep_ms = sum(a.elapsed_time(z) for a, z in evs) / (args.steps * (ips - 1))
+    plain_ms, plain_sweeps = eng.timing(0)
+    sweep_ms = plain_ms / max(plain_sweeps, 1)
     t = torch.tensor([ms, sweep_ms], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -320,7 +314,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "secondary": secondary,
-            "gpu_launches": args.steps * (ips - 1 + 3),
+            # sweeps + one reduction per check + the initial and final evaluate/reduce
+            "gpu_launches": args.steps * ips + args.steps + 3,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

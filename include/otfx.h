@@ -184,6 +184,11 @@ int otfx_nccl_unique_id(unsigned char id[128]);
  * allreduces the check scalars */
 int otfx_engine_attach_nccl(otfx_engine* e, const unsigned char id[128], int nranks, int rank);
 
+/* device time of the plain-iteration graph launches (CUDA events on the
+ * engine stream): returns the time / sweep count accumulated so far, then
+ * enable = 1 resets and starts, 0 resets and stops, -1 leaves it running */
+int otfx_engine_timing(otfx_engine* e, int enable, double* plain_ms, int64_t* plain_sweeps);
+
 /* enqueue-side helpers for timing */
 int otfx_engine_sync(otfx_engine* e);
 void* otfx_engine_stream(otfx_engine* e);

@@ -67,8 +67,9 @@ struct SweepArgs {
   T den_u, den_w;        // (1 + 2 mu eps), (1 + 2 thr_w eps/alpha); 1 when eps == 0
   int has_eps;
   double alpha, eps;
-  double* partials;      // [gridDim.x*gridDim.y][R_NSUM] (CHECK sweeps / evaluate)
-  double* maxes;         // [gridDim.x*gridDim.y][2]
+  double* partials;      // CHECK sweeps: [blocks][10]; evaluate: [blocks][8]
+  double* maxes;         // evaluate: [blocks][2]
+  double* dualp;         // DUAL sweeps: [blocks][4] = PENU, PENW, GU, GW
   double coef[MAX_CHAN_COEF];  // graph D/c (k x ell, row-major) or Lindblad (ell,k,k,{re,im})
 };
 

@@ -191,7 +191,7 @@ __global__ void reduce_raw_kernel(const double* __restrict__ pe, const double* _
   }
   if (with_res) {
     for (int b = threadIdx.x; b < nbs; b += blockDim.x) {
-      for (int q = 0; q < 4; ++q) v[8 + q] += ps[b * 4 + q];
+      for (int q = 0; q < 4; ++q) v[8 + q] += ps[b * 10 + q];
     }
   }
   double mx[2] = {0.0, 0.0};
@@ -205,6 +205,40 @@ __global__ void reduce_raw_kernel(const double* __restrict__ pe, const double* _
   block_max<2>(mx, sred);
   if (threadIdx.x == 0) {
     for (int q = 0; q < 12; ++q) raw[q] = s12[q];
+    raw[R_GU] = mx[0];
+    raw[R_GW] = mx[1];
+  }
+}
+
+// Fused check: R^k, primal and feasibility partials of the check sweep
+// ([nb][10]) and the dual-norm partials of the following sweep ([nb][4]).
+__global__ void reduce_fused_kernel(const double* __restrict__ pc, const double* __restrict__ pd,
+                                    int nb, double* raw) {
+  __shared__ double sred[32 * 12];
+  double v[12], mx[2] = {0.0, 0.0};
+  for (int q = 0; q < 12; ++q) v[q] = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const double* c = pc + size_t(b) * 10;
+    const double* d = pd + size_t(b) * 4;
+    v[R_SDU] += c[0];
+    v[R_SDW] += c[1];
+    v[R_SDPHI] += c[2];
+    v[R_SCROSS] += c[3];
+    v[R_PU] += c[4];
+    v[R_PW] += c[5];
+    v[R_SU2] += c[6];
+    v[R_SW2] += c[7];
+    v[R_SCON] += c[8];
+    v[R_SPHID] += c[9];
+    v[R_PENU] += d[0];
+    v[R_PENW] += d[1];
+    mx[0] = dmax(mx[0], d[2]);
+    mx[1] = dmax(mx[1], d[3]);
+  }
+  block_sum<12>(v, sred);
+  block_max<2>(mx, sred);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 12; ++q) raw[q] = v[q];
     raw[R_GU] = mx[0];
     raw[R_GW] = mx[1];
   }
@@ -242,7 +276,8 @@ struct otfx_engine {
   int TX = 128, R = 64, gx = 1, gy = 1;
   size_t smem_plain = 0, smem_check = 0;
   // reductions
-  double* d_part_sweep = nullptr;  // [gx*gy][4]
+  double* d_part_sweep = nullptr;  // [gx*gy][10] check-sweep partials
+  double* d_part_dual = nullptr;   // [gx*gy][4] dual-sweep partials
   double* d_part_eval = nullptr;   // [ex*ey][8]
   double* d_max_eval = nullptr;    // [ex*ey][2]
   double* d_raw = nullptr;         // [OTFX_NRAW]
@@ -255,6 +290,12 @@ struct otfx_engine {
   size_t stage_bytes = 0;
   double* d_pack_part = nullptr;
   double* h_pack_part = nullptr;
+  // device-side timing of the plain-iteration graphs (for the bench roofline)
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  std::vector<std::pair<int, int64_t>> ev_pending;  // (pool index, sweeps)
+  double plain_ms = 0.0;
+  int64_t plain_sweeps = 0;
   // graphs
   bool use_graphs = true;
   std::map<std::pair<int, int64_t>, cudaGraphExec_t> graphs;
@@ -307,6 +348,7 @@ static SweepArgs<T> make_args(otfx_engine* e, int from) {
   a.eps = eps;
   a.partials = e->d_part_sweep;
   a.maxes = nullptr;
+  a.dualp = e->d_part_dual;
   const int K = e->K;
   if (e->d.kind == OTFX_KIND_VECTOR) {
     const int L = e->LMAX;
@@ -325,15 +367,18 @@ const Ops<double>* ops_of<double>(otfx_engine* e) { return e->ops64; }
 template <>
 const Ops<float>* ops_of<float>(otfx_engine* e) { return e->ops32; }
 
+// fl bit 0: check sweep; bit 1: dual-norm accumulation (TMA sweep only)
 template <typename T>
-static void launch_sweep(otfx_engine* e, bool check) {
+static void launch_sweep(otfx_engine* e, int fl) {
   if (e->use_tma) {
     TmaSweepArgs<T> g;
     g.s = make_args<T>(e, e->cur);
     g.L = e->L;
     CK(ops_of<T>(e)->sweep_tma(g, e->maps[e->cur], dim3(e->gx, e->gy), dim3(32 * (e->L.cw + 1)),
-                               e->stream, check));
+                               e->stream, fl));
   } else {
+    require((fl & 2) == 0, OTFX_EINVAL, "dual accumulation needs the TMA sweep");
+    const bool check = (fl & 1) != 0;
     SweepArgs<T> a = make_args<T>(e, e->cur);
     CK(ops_of<T>(e)->sweep(a, dim3(e->gx, e->gy), dim3(e->TX),
                            check ? e->smem_check : e->smem_plain, e->stream, check));
@@ -401,9 +446,9 @@ static bool plan_stages(otfx_engine* e, int S) {
   return L.total <= 227 * 1024;
 }
 
-static void launch_sweep(otfx_engine* e, bool check) {
-  if (e->elem == 8) launch_sweep<double>(e, check);
-  else launch_sweep<float>(e, check);
+static void launch_sweep(otfx_engine* e, int fl) {
+  if (e->elem == 8) launch_sweep<double>(e, fl);
+  else launch_sweep<float>(e, fl);
 }
 
 template <typename T>
@@ -482,7 +527,7 @@ static int env_int(const char* name, int dflt) {
 
 static void enqueue_plain(otfx_engine* e, int64_t count) {
   for (int64_t q = 0; q < count; ++q) {
-    launch_sweep(e, false);
+    launch_sweep(e, 0);
     exchange_nccl(e);
   }
 }
@@ -515,8 +560,34 @@ static void run_plain(otfx_engine* e, int64_t count) {
     cudaGraphDestroy(g);
     it = e->graphs.emplace(key, ge).first;
   }
+  int slot = -1;
+  if (e->timing) {
+    slot = int(e->ev_pending.size());
+    while (int(e->ev_pool.size()) <= slot) {
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      e->ev_pool.emplace_back(a, b);
+    }
+    CK(cudaEventRecord(e->ev_pool[slot].first, e->stream));
+  }
   CK(cudaGraphLaunch(it->second, e->stream));
+  if (e->timing) {
+    CK(cudaEventRecord(e->ev_pool[slot].second, e->stream));
+    e->ev_pending.emplace_back(slot, count);
+  }
   e->cur ^= int(count & 1);
+}
+
+// fold the timed graph launches into plain_ms once the stream has caught up
+static void collect_timing(otfx_engine* e) {
+  for (auto& pr : e->ev_pending) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e->ev_pool[pr.first].first, e->ev_pool[pr.first].second));
+    e->plain_ms += ms;
+    e->plain_sweeps += pr.second;
+  }
+  e->ev_pending.clear();
 }
 
 // raw scalars of the current iterate into d_raw (and h_raw after sync)
@@ -537,6 +608,27 @@ static void raw_to_host(otfx_engine* e, bool with_res, bool allreduce) {
   CK(cudaMemcpyAsync(e->h_raw, e->d_raw, OTFX_NRAW * sizeof(double), cudaMemcpyDeviceToHost,
                      e->stream));
   CK(cudaStreamSynchronize(e->stream));
+  collect_timing(e);
+}
+
+// fused check: the check sweep already wrote R^k + primal/feasibility
+// partials, the speculative sweep after it the dual-norm partials
+static void raw_fused_to_host(otfx_engine* e) {
+  reduce_fused_kernel<<<1, 256, 0, e->stream>>>(e->d_part_sweep, e->d_part_dual, e->gx * e->gy,
+                                                 e->d_raw);
+  CK(cudaGetLastError());
+  if (e->comm && e->nranks > 1) {
+    NcclApi& N = nccl();
+    NK(N.GroupStart());
+    NK(N.AllReduce(e->d_raw, e->d_raw, OTFX_NRAW_SUM, ncclFloat64, ncclSum, e->comm, e->stream));
+    NK(N.AllReduce(e->d_raw + OTFX_NRAW_SUM, e->d_raw + OTFX_NRAW_SUM, OTFX_NRAW - OTFX_NRAW_SUM,
+                   ncclFloat64, ncclMax, e->comm, e->stream));
+    NK(N.GroupEnd());
+  }
+  CK(cudaMemcpyAsync(e->h_raw, e->d_raw, OTFX_NRAW * sizeof(double), cudaMemcpyDeviceToHost,
+                     e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  collect_timing(e);
 }
 
 // S/solver.py:242-291 scalar algebra, same operation order
@@ -1011,8 +1103,8 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   const int max_rec = std::max(2 * e->K * e->K * std::max(1, d->ell) * 2, 16);
   e->stage_bytes = std::max<size_t>(size_t(128) << 20, size_t(4) * n * max_rec * sizeof(double));
 
-  const size_t n_sweep = size_t(e->gx) * e->gy * 4, n_pe = size_t(e->ex) * e->ey * 8,
-               n_me = size_t(e->ex) * e->ey * 2;
+  const size_t n_sweep = size_t(e->gx) * e->gy * 10, n_pe = size_t(e->ex) * e->ey * 8,
+               n_me = size_t(e->ex) * e->ey * 2, n_du = size_t(e->gx) * e->gy * 4;
   const size_t halo = size_t(8) * NP * n * e->elem;
   size_t off = 0;
   auto carve = [&](size_t bytes) {
@@ -1023,6 +1115,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   const size_t o_state0 = carve(e->state_bytes), o_state1 = carve(e->state_bytes);
   const size_t o_diff = carve(size_t(NP) * pb);
   const size_t o_ps = carve(n_sweep * 8), o_pe = carve(n_pe * 8), o_me = carve(n_me * 8);
+  const size_t o_du = carve(n_du * 8);
   const size_t o_raw = carve(64 * 8);
   const size_t o_pack = carve(kPackBlocks * 3 * 8);
   const size_t o_halo = carve(halo);
@@ -1038,6 +1131,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   }
   e->diff = e->mem + o_diff;
   e->d_part_sweep = reinterpret_cast<double*>(e->mem + o_ps);
+  e->d_part_dual = reinterpret_cast<double*>(e->mem + o_du);
   e->d_part_eval = reinterpret_cast<double*>(e->mem + o_pe);
   e->d_max_eval = reinterpret_cast<double*>(e->mem + o_me);
   e->d_raw = reinterpret_cast<double*>(e->mem + o_raw);
@@ -1062,6 +1156,10 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
 static void destroy(otfx_engine* e) {
   if (!e) return;
   drop_graphs(e);
+  for (auto& pr : e->ev_pool) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
   if (e->stream) cudaStreamSynchronize(e->stream);
   if (e->comm && nccl().CommDestroy) nccl().CommDestroy(e->comm);
   if (e->mem) cudaFree(e->mem);
@@ -1262,7 +1360,7 @@ int otfx_engine_sweep(otfx_engine* e, int check) {
   API_BEGIN
   require(e, OTFX_EINVAL, "null engine");
   CK(cudaSetDevice(e->d.device));
-  launch_sweep(e, check != 0);
+  launch_sweep(e, check != 0 ? 1 : 0);
   e->residual_valid = check != 0;
   API_END
 }
@@ -1282,7 +1380,7 @@ int otfx_engine_step_check(otfx_engine* e, double out[5]) {
   API_BEGIN
   require(e && out, OTFX_EINVAL, "null pointer");
   CK(cudaSetDevice(e->d.device));
-  launch_sweep(e, true);
+  launch_sweep(e, 1);
   exchange_nccl(e);
   raw_to_host(e, true, true);
   finalize(e, e->h_raw, out);
@@ -1327,17 +1425,33 @@ int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_poi
   bool conv = r[2] <= cfg->tol_gap && r[3] <= cfg->tol_feas;
   int64_t it = 0;
   const int64_t ce = cfg->check_every, mx = cfg->max_iters;
+  const bool fused_ok = e->use_tma && env_int("OTFX_FUSED_CHECK", 1) != 0;
   while (!conv && it < mx) {
     const int64_t next = std::min((it / ce + 1) * ce, mx);
     run_plain(e, next - it - 1);
     it = next - 1;
-    launch_sweep(e, true);
+    // Fused check: the iteration after the check runs speculatively and
+    // accumulates the dual norms of the checked iterate; it is kept when the
+    // run continues and dropped (ping-pong buffer flipped back) when it stops.
+    // It must not itself be a check iteration.
+    const bool fuse = fused_ok && next + 1 < mx && (next + 1) % ce != 0;
+    launch_sweep(e, 1);
     exchange_nccl(e);
-    raw_to_host(e, true, true);
+    if (fuse) {
+      launch_sweep(e, 2);
+      exchange_nccl(e);
+      raw_fused_to_host(e);
+    } else {
+      raw_to_host(e, true, true);
+    }
     finalize(e, e->h_raw, r);
-    ++it;
+    it = next;
     push(it, r, r[4]);
     conv = r[2] <= cfg->tol_gap && r[3] <= cfg->tol_feas;
+    if (fuse) {
+      if (conv) e->cur ^= 1;  // drop the speculative iterate
+      else ++it;              // keep it: iteration next+1 is done
+    }
   }
   *n_history = nh;
   *iterations = it;
@@ -1434,6 +1548,22 @@ int otfx_engine_attach_nccl(otfx_engine* e, const unsigned char id[128], int nra
   e->nranks = nranks;
   e->rank = rank;
   drop_graphs(e);
+  API_END
+}
+
+int otfx_engine_timing(otfx_engine* e, int enable, double* plain_ms, int64_t* plain_sweeps) {
+  API_BEGIN
+  require(e, OTFX_EINVAL, "null engine");
+  CK(cudaStreamSynchronize(e->stream));
+  collect_timing(e);
+  // report what was accumulated so far, then (enable >= 0) reset and start/stop
+  if (plain_ms) *plain_ms = e->plain_ms;
+  if (plain_sweeps) *plain_sweeps = e->plain_sweeps;
+  if (enable >= 0) {
+    e->timing = enable != 0;
+    e->plain_ms = 0.0;
+    e->plain_sweeps = 0;
+  }
   API_END
 }
 

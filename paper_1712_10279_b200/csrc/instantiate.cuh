@@ -16,24 +16,28 @@ struct OpsFor {
     e = cudaFuncSetAttribute(sweep_kernel<P, T, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(sweep_tma_kernel<P, T, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(sweep_tma_kernel<P, T, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    const void* tk[4] = {(const void*)sweep_tma_kernel<P, T, 0>, (const void*)sweep_tma_kernel<P, T, 1>,
+                         (const void*)sweep_tma_kernel<P, T, 2>, (const void*)sweep_tma_kernel<P, T, 3>};
+    for (int q = 0; q < 4; ++q) {
+      e = cudaFuncSetAttribute(tk[q], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
   }
   static cudaError_t sweep_tma(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
-                               cudaStream_t s, bool check) {
-    if (check)
-      sweep_tma_kernel<P, T, true><<<g, b, a.L.total, s>>>(a, m);
-    else
-      sweep_tma_kernel<P, T, false><<<g, b, a.L.total, s>>>(a, m);
+                               cudaStream_t s, int fl) {
+    switch (fl & 3) {
+      case 0: sweep_tma_kernel<P, T, 0><<<g, b, a.L.total, s>>>(a, m); break;
+      case 1: sweep_tma_kernel<P, T, 1><<<g, b, a.L.total, s>>>(a, m); break;
+      case 2: sweep_tma_kernel<P, T, 2><<<g, b, a.L.total, s>>>(a, m); break;
+      default: sweep_tma_kernel<P, T, 3><<<g, b, a.L.total, s>>>(a, m); break;
+    }
     return cudaGetLastError();
   }
   static int tma_regs(bool check) {
     cudaFuncAttributes at;
-    if (check) cudaFuncGetAttributes(&at, sweep_tma_kernel<P, T, true>);
-    else cudaFuncGetAttributes(&at, sweep_tma_kernel<P, T, false>);
+    if (check) cudaFuncGetAttributes(&at, sweep_tma_kernel<P, T, 1>);
+    else cudaFuncGetAttributes(&at, sweep_tma_kernel<P, T, 0>);
     return at.numRegs;
   }
   static cudaError_t sweep(const SweepArgs<T>& a, dim3 g, dim3 b, size_t smem, cudaStream_t s,

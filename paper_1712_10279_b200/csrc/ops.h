@@ -21,8 +21,9 @@ struct Ops {
                        bool check);
   cudaError_t (*evaluate)(const SweepArgs<T>& a, dim3 grid, dim3 block, cudaStream_t s);
   cudaError_t (*residual)(const SweepArgs<T>& a, dim3 grid, dim3 block, cudaStream_t s);
+  // fl bit 0: check sweep (R^k + primal/feasibility), bit 1: dual-norm sweep
   cudaError_t (*sweep_tma)(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 grid, dim3 block,
-                           cudaStream_t s, bool check);
+                           cudaStream_t s, int fl);
   int (*sweep_regs)(bool check);
   int (*tma_regs)(bool check);
 };

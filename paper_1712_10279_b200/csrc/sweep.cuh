@@ -47,6 +47,28 @@ struct Cell {
     }
     P::prox_u(un, A);
   }
+  // forward-difference gradient with zero ghost entries (S/spatial.py:80-86)
+  template <class PA>
+  __device__ static __forceinline__ void grad(const T (&ph)[NP], const T (&phx)[NP],
+                                              const T (&phy)[NP], bool hasx, bool hasy,
+                                              T (&g)[2][NP], const PA& A) {
+#pragma unroll
+    for (int c = 0; c < NP; ++c) {
+      g[0][c] = hasx ? (phx[c] - ph[c]) * A.inv_dx : T(0);
+      g[1][c] = hasy ? (phy[c] - ph[c]) * A.inv_dx : T(0);
+    }
+  }
+  // u' = prox_u(g mu + u)  (S/solver.py:221-224)
+  template <class PA>
+  __device__ static __forceinline__ void flux_g(const T (&g)[2][NP], const T (&uo)[2][NP],
+                                                T (&un)[2][NP], const PA& A) {
+#pragma unroll
+    for (int c = 0; c < NP; ++c) {
+      un[0][c] = g[0][c] * A.mu + uo[0][c];
+      un[1][c] = g[1][c] * A.mu + uo[1][c];
+    }
+    P::prox_u(un, A);
+  }
 };
 
 template <typename T>
@@ -298,9 +320,11 @@ __global__ void __launch_bounds__(128) sweep_kernel(const __grid_constant__ Swee
   if (CHECK) {
     block_sum<4>(acc, sred);
     if (t == 0) {
-      double* dst = A.partials + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * 4;
+      double* dst = A.partials + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * 10;
 #pragma unroll
       for (int s = 0; s < 4; ++s) dst[s] = acc[s];
+#pragma unroll
+      for (int s = 4; s < 10; ++s) dst[s] = 0.0;
     }
   }
 }

@@ -104,9 +104,17 @@ struct StageShape {
   static constexpr int BYTES = OFF_P + R128(P::NP * ROW);
 };
 
-template <class P, typename T, bool CHECK>
+// FL bit 0 (CHECK): this sweep ends on a check iteration -- accumulate the
+//   R^k terms plus the primal, feasibility and <phi, diff> terms of the new
+//   iterate (S/solver.py:242-256, 282-291) from registers;
+// FL bit 1 (DUAL): the INPUT iterate is a checked one -- accumulate the dual
+//   norms of its gradients (S/solver.py:258-274), which this sweep computes
+//   anyway for the flux and channel updates.
+template <class P, typename T, int FL>
 __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ TmaSweepArgs<T> G,
                                                        const __grid_constant__ TmaSet M) {
+  constexpr bool CHECK = (FL & 1) != 0;
+  constexpr bool DUAL = (FL & 2) != 0;
   using SS = StageShape<P, T>;
   constexpr int NP = P::NP;
   constexpr int NWA = P::NWA;
@@ -144,7 +152,9 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
   }
   __syncthreads();
 
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  // CHECK: SDU SDW SDPHI SCROSS PU PW SU2 SW2 SCON SPHID;  DUAL: PENU PENW | GU GW
+  double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double dsum[2] = {0.0, 0.0}, dmx[2] = {0.0, 0.0};
   if (producer) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
@@ -205,11 +215,12 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
                      : "memory");
     };
-    T uxb_prev[NP], dux_prev[NP];
+    T uxb_prev[NP], dux_prev[NP], unx_prev[NP];
 #pragma unroll
     for (int c = 0; c < NP; ++c) {
       uxb_prev[c] = T(0);
       dux_prev[c] = T(0);
+      unx_prev[c] = T(0);
     }
     int s1 = 1, ph1 = 0;  // cursor of stage q+1
     if (S == 1) s1 = 0;
@@ -234,6 +245,7 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
       for (int c = 0; c < NP; ++c) {
         uxb_prev[c] = (un[0][c] + un[0][c]) - uo[0][c];
         dux_prev[c] = un[0][c] - uo[0][c];
+        unx_prev[c] = un[0][c];
       }
     }
     release(s0);
@@ -256,9 +268,9 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
       const T* sD = reinterpret_cast<const T*>(st0 + SS::OFF_D);
       const T* sP = reinterpret_cast<const T*>(st0 + SS::OFF_P);
       const T* sPn = reinterpret_cast<const T*>(st1 + SS::OFF_P);
-      T phc[NP], un[2][NP], ub[2][NP], uo[2][NP], lub[NP], ldu[NP];
+      T phc[NP], un[2][NP], ub[2][NP], uo[2][NP], lub[NP], ldu[NP], lun[NP];
       {
-        T phx[NP], phy[NP];
+        T phx[NP], phy[NP], g[2][NP];
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
           phc[c] = sP[c * TW];
@@ -267,14 +279,19 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
           uo[0][c] = sU[c * TW];
           uo[1][c] = sU[(NP + c) * TW];
         }
-        Cell<P, T>::flux(phc, phx, phy, hasx, hasy, uo, un, H);
+        Cell<P, T>::grad(phc, phx, phy, hasx, hasy, g, H);
+        if (DUAL && out) P::dual_u(g, H.norm_u, dmx[0], dsum[0]);
+        Cell<P, T>::flux_g(g, uo, un, H);
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
           ub[0][c] = (un[0][c] + un[0][c]) - uo[0][c];
           ub[1][c] = (un[1][c] + un[1][c]) - uo[1][c];
-          // ubar_y / du_y of the left neighbour (i, j-1) from lane - 1
+          // ubar_y / du_y / u'_y of the left neighbour (i, j-1) from lane - 1
           lub[c] = __shfl_up_sync(0xffffffffu, ub[1][c], 1);
-          if (CHECK) ldu[c] = __shfl_up_sync(0xffffffffu, un[1][c] - uo[1][c], 1);
+          if (CHECK) {
+            ldu[c] = __shfl_up_sync(0xffffffffu, un[1][c] - uo[1][c], 1);
+            lun[c] = __shfl_up_sync(0xffffffffu, un[1][c], 1);
+          }
         }
       }
       T df[NP], wo[NWA];
@@ -301,6 +318,7 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
         if (P::HAS_W) {
           T gc[NWA];
           P::grad_c(phc, gc, H);
+          if (DUAL) P::dual_w(gc, H.norm_w, H.ell, H.alpha, dmx[1], dsum[1]);
 #pragma unroll
           for (int e = 0; e < NWA; ++e) wn[e] = gc[e] * H.nu + wo[e];
           P::prox_w(wn, H);
@@ -361,12 +379,48 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
             acc[2] += P::wp(c) * double(dp) * double(dp);
             acc[3] += P::wp(c) * double(dp) * double(cross[c]);
           }
+          // primal / feasibility / <phi, diff> of the new iterate
+          acc[4] += P::norm_u(un, H.norm_u);
+          T con[NP];
+          double su = 0.0, sc2 = 0.0, sp = 0.0;
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            su += P::wp(c) * (double(un[0][c]) * double(un[0][c]) +
+                              double(un[1][c]) * double(un[1][c]));
+            T d = un[0][c];
+            if (i > 0) d = d - unx_prev[c];
+            d = d + un[1][c];
+            if (j > 0) d = d - lun[c];
+            con[c] = d * H.inv_dx - df[c];
+          }
+          acc[6] += su;
+          if (P::HAS_W) {
+            acc[5] += P::norm_w(wn, H.norm_w);
+            double sw = 0.0;
+#pragma unroll
+            for (int e = 0; e < NWA; ++e) sw += P::ww(e) * double(wn[e]) * double(wn[e]);
+            acc[7] += sw;
+            T dv[NP];
+            P::div_c(wn, dv, H);
+#pragma unroll
+            for (int c = 0; c < NP; ++c) con[c] = con[c] + dv[c];
+          }
+#pragma unroll
+          for (int c = 0; c < NP; ++c) {
+            sc2 += P::wp(c) * double(con[c]) * double(con[c]);
+            sp += P::wp(c) * double(phnew[c]) * double(df[c]);
+          }
+          acc[8] += sc2;
+          acc[9] += sp;
         }
       }
 #pragma unroll
       for (int c = 0; c < NP; ++c) {
         uxb_prev[c] = ub[0][c];
-        if (CHECK) dux_prev[c] = un[0][c] - uo[0][c];
+        if (CHECK) {
+          dux_prev[c] = un[0][c] - uo[0][c];
+          unx_prev[c] = un[0][c];
+        }
       }
       s0 = s1;
       ph0 = ph1;
@@ -374,12 +428,24 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
     }
   }
 
+  const size_t bid = size_t(blockIdx.y) * gridDim.x + blockIdx.x;
   if (CHECK) {
-    block_sum<4>(acc, sred);
+    block_sum<10>(acc, sred);
     if (t == 0) {
-      double* dst = A.partials + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * 4;
+      double* dst = A.partials + bid * 10;
 #pragma unroll
-      for (int s = 0; s < 4; ++s) dst[s] = acc[s];
+      for (int s = 0; s < 10; ++s) dst[s] = acc[s];
+    }
+  }
+  if (DUAL) {
+    block_sum<2>(dsum, sred);
+    block_max<2>(dmx, sred);
+    if (t == 0) {
+      double* dst = A.dualp + bid * 4;
+      dst[0] = dsum[0];
+      dst[1] = dsum[1];
+      dst[2] = dmx[0];
+      dst[3] = dmx[1];
     }
   }
 }

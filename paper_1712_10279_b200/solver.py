@@ -318,6 +318,13 @@ class CudaEngine:
             self._h, raw.ctypes.data_as(C.POINTER(C.c_double)), out))
         return tuple(out)
 
+    def timing(self, enable=-1):
+        """Device time of the plain-iteration graphs since the last reset:
+        enable=1 reset+start, 0 reset+stop, -1 read.  Returns (ms, sweeps)."""
+        ms, cnt = C.c_double(), C.c_int64()
+        _lib.check(self._lib.otfx_engine_timing(self._h, int(enable), C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
     def sync(self):
         _lib.check(self._lib.otfx_engine_sync(self._h))
 
