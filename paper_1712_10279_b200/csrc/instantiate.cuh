@@ -4,6 +4,7 @@
 #include "ops.h"
 #include "sweep.cuh"
 #include "sweep_tma.cuh"
+#include "sweep_tb2.cuh"
 
 namespace otfx {
 
@@ -22,7 +23,18 @@ struct OpsFor {
       e = cudaFuncSetAttribute(tk[q], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       if (e != cudaSuccess) return e;
     }
-    return cudaSuccess;
+    return cudaFuncSetAttribute(sweep_tb2_kernel<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024);
+  }
+  static cudaError_t sweep_tb2(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
+                               cudaStream_t s) {
+    sweep_tb2_kernel<P, T><<<g, b, a.L.total, s>>>(a, m);
+    return cudaGetLastError();
+  }
+  static int tb2_regs() {
+    cudaFuncAttributes at;
+    cudaFuncGetAttributes(&at, sweep_tb2_kernel<P, T>);
+    return at.numRegs;
   }
   static cudaError_t sweep_tma(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
                                cudaStream_t s, int fl) {
@@ -65,7 +77,7 @@ struct OpsFor {
   static const Ops<T>* table(int kind) {
     static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
                              P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &sweep_tma,
-                             &regs,    &tma_regs};
+                             &sweep_tb2, &regs, &tma_regs, &tb2_regs};
     return &o;
   }
 };

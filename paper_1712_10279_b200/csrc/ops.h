@@ -5,6 +5,7 @@
 
 #include "common.cuh"
 #include "sweep_tma.cuh"
+#include "sweep_tb2.cuh"
 
 namespace otfx {
 
@@ -24,8 +25,12 @@ struct Ops {
   // fl bit 0: check sweep (R^k + primal/feasibility), bit 1: dual-norm sweep
   cudaError_t (*sweep_tma)(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 grid, dim3 block,
                            cudaStream_t s, int fl);
+  // two iterations per pass (temporal blocking); plain iterations only
+  cudaError_t (*sweep_tb2)(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 grid, dim3 block,
+                           cudaStream_t s);
   int (*sweep_regs)(bool check);
   int (*tma_regs)(bool check);
+  int (*tb2_regs)();
 };
 
 // registries, one per instantiation unit

@@ -47,6 +47,7 @@ struct VecPolicy {
   static constexpr int NW = HASW ? LMAX : 0;
   static constexpr int NWA = HASW ? LMAX : 1;   // array extent
   static constexpr bool HAS_W = HASW;
+  static constexpr int NCOEF = K * LMAX;        // graph D/c entries the kernels read
 
   __device__ static __forceinline__ double wp(int) { return 1.0; }
   __device__ static __forceinline__ double ww(int) { return 1.0; }
@@ -433,6 +434,7 @@ struct SymPolicy {
   static constexpr int NW = LMAX * NWS;
   static constexpr int NWA = NW;
   static constexpr bool HAS_W = true;
+  static constexpr int NCOEF = 0;  // Lindblad stack stays in parameter space
 
   __device__ static __forceinline__ double wp(int i) { return i < K ? 1.0 : 2.0; }
   __device__ static __forceinline__ double ww(int) { return 2.0; }
@@ -665,6 +667,7 @@ struct HermPolicy {
   static constexpr int NW = LMAX * NWS;
   static constexpr int NWA = NW;
   static constexpr bool HAS_W = true;
+  static constexpr int NCOEF = 0;  // Lindblad stack stays in parameter space
 
   __device__ static __forceinline__ double wp(int i) { return i < K ? 1.0 : 2.0; }
   __device__ static __forceinline__ double ww(int i) { return (i % NWS) < K ? 1.0 : 2.0; }

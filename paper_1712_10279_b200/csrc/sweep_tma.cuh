@@ -56,14 +56,14 @@ struct TmaSweepArgs {
 // Channel coefficients as the kernels read them: the small vector D/c matrix
 // is pulled into registers once per CTA; the Lindblad stacks stay in the
 // (constant-cached) parameter space.
-template <class P, typename T, bool REG = (P::NWS == 1)>
+template <class P, typename T, bool REG = (P::NCOEF > 0)>
 struct CoefView;
 template <class P, typename T>
 struct CoefView<P, T, true> {
-  T c[P::K * P::LMAX];
+  T c[P::NCOEF];
   __device__ __forceinline__ void load(const SweepArgs<T>& A) {
 #pragma unroll
-    for (int q = 0; q < P::K * P::LMAX; ++q) c[q] = T(A.coef[q]);
+    for (int q = 0; q < P::NCOEF; ++q) c[q] = T(A.coef[q]);
   }
   __device__ __forceinline__ T operator[](int q) const { return c[q]; }
 };
