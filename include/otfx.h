@@ -111,6 +111,9 @@ typedef struct {
   int32_t graphs;        /* CUDA graphs in use */
   int32_t tma_stages;    /* TMA ring depth of the streamed sweep (0: register sweep) */
   int32_t smem_bytes;    /* dynamic shared memory per sweep CTA */
+  int32_t tb2;           /* plain iterations run two per HBM pass (temporal blocking) */
+  int32_t regs_tb2;      /* registers per thread of the two-level sweep */
+  int32_t smem_tb2;      /* dynamic shared memory per two-level CTA */
 } otfx_engine_info;
 
 int otfx_abi_version(void);

@@ -48,7 +48,8 @@ class EngineInfo(C.Structure):
                 ("np", C.c_int32), ("nws", C.c_int32), ("lmax", C.c_int32), ("pitch", C.c_int32),
                 ("tile_cols", C.c_int32), ("tile_rows", C.c_int32), ("grid_x", C.c_int32),
                 ("grid_y", C.c_int32), ("regs_plain", C.c_int32), ("regs_check", C.c_int32),
-                ("graphs", C.c_int32), ("tma_stages", C.c_int32), ("smem_bytes", C.c_int32)]
+                ("graphs", C.c_int32), ("tma_stages", C.c_int32), ("smem_bytes", C.c_int32),
+                ("tb2", C.c_int32), ("regs_tb2", C.c_int32), ("smem_tb2", C.c_int32)]
 
 
 _P = C.c_void_p

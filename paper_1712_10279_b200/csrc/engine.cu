@@ -307,6 +307,11 @@ struct otfx_engine {
   bool use_tma = false;
   otfx::StageLayout L{};
   otfx::TmaSet maps[2];
+  // temporal blocking: two iterations per pass (single-slab engines)
+  bool use_tb2 = false;
+  otfx::StageLayout L2{};
+  otfx::TmaSet maps2[2];
+  int gx2 = 1, gy2 = 1;
   // policy dispatch
   const otfx::Ops<double>* ops64 = nullptr;
   const otfx::Ops<float>* ops32 = nullptr;
@@ -402,13 +407,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // 3-D view (cols = n, rows = rows_alloc, planes) of a group of planes; one box
 // = L.tw columns x 1 row x all planes; columns outside [0, n) read as zero
-static void make_map(otfx_engine* e, CUtensorMap* m, void* base, int planes) {
+static void make_map(otfx_engine* e, CUtensorMap* m, void* base, int planes, int tw) {
   memset(m, 0, sizeof(*m));
   if (planes <= 0) return;
   require(planes <= 256, OTFX_EUNSUPPORTED, "too many planes for one TMA box");
   cuuint64_t dims[3] = {cuuint64_t(e->d.n), cuuint64_t(e->rows_alloc), cuuint64_t(planes)};
   cuuint64_t strides[2] = {cuuint64_t(e->pitch) * e->elem, cuuint64_t(e->plane) * e->elem};
-  cuuint32_t box[3] = {cuuint32_t(e->L.tw), 1u, cuuint32_t(planes)};
+  cuuint32_t box[3] = {cuuint32_t(tw), 1u, cuuint32_t(planes)};
   cuuint32_t es[3] = {1u, 1u, 1u};
   CUresult r = tensor_map_encoder()(
       m, e->elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base,
@@ -442,13 +447,54 @@ static bool plan_stages(otfx_engine* e, int S) {
   L.off_stages = 128;
   L.off_xchg = L.off_stages + S * L.stage_bytes;
   L.off_red = round_up(L.off_xchg, 16);
-  L.total = L.off_red + 32 * 4 * 8;
+  L.total = L.off_red + 32 * 10 * 8;
+  return L.total <= 227 * 1024;
+}
+
+// shared-memory plan of the two-level sweep (same formulas as TB2Shape<P,T>)
+static bool plan_tb2(otfx_engine* e, int S) {
+  StageLayout& L = e->L2;
+  require(S >= 3 && S <= 8, OTFX_EINVAL, "TMA ring depth must be in [3, 8]");
+  L.cw = 4;
+  L.tile = 29 * 4;
+  L.h = 16 / e->elem;
+  L.tw = ((118 + L.h) + L.h - 1) / L.h * L.h;
+  L.S = S;
+  const int row = L.tw * e->elem;
+  const int bu = 2 * e->NP * row, bw = e->NWact * row, bd = e->NP * row, bp = e->NP * row;
+  const int nwcap = e->has_w ? e->LMAX * e->NWS : 1;
+  L.off_w = round_up(bu, 128);
+  L.off_d = L.off_w + round_up(nwcap * row, 128);
+  L.off_p = L.off_d + round_up(bd, 128);
+  L.stage_bytes = L.off_p + round_up(bp, 128);
+  L.bytes_full = bu + bw + bd + bp;
+  L.bytes_flux = bu + bp;
+  L.bytes_phi = bp;
+  L.off_stages = 128;
+  L.off_xchg = L.off_stages + S * L.stage_bytes;
+  L.off_red = round_up(L.off_xchg, 16);
+  L.total = L.off_red;
   return L.total <= 227 * 1024;
 }
 
 static void launch_sweep(otfx_engine* e, int fl) {
   if (e->elem == 8) launch_sweep<double>(e, fl);
   else launch_sweep<float>(e, fl);
+}
+
+// two plain iterations in one pass (sweep_tb2_kernel)
+template <typename T>
+static void launch_tb2(otfx_engine* e) {
+  TmaSweepArgs<T> g;
+  g.s = make_args<T>(e, e->cur);
+  g.L = e->L2;
+  CK(ops_of<T>(e)->sweep_tb2(g, e->maps2[e->cur], dim3(e->gx2, e->gy2), dim3(160), e->stream));
+  e->cur ^= 1;
+}
+
+static void launch_tb2(otfx_engine* e) {
+  if (e->elem == 8) launch_tb2<double>(e);
+  else launch_tb2<float>(e);
 }
 
 template <typename T>
@@ -526,10 +572,19 @@ static int env_int(const char* name, int dflt) {
 }
 
 static void enqueue_plain(otfx_engine* e, int64_t count) {
-  for (int64_t q = 0; q < count; ++q) {
+  int64_t q = 0;
+  if (e->use_tb2) {
+    for (; q + 2 <= count; q += 2) launch_tb2(e);
+  }
+  for (; q < count; ++q) {
     launch_sweep(e, 0);
     exchange_nccl(e);
   }
+}
+
+// buffer flips of enqueue_plain(count)
+static int64_t plain_flips(const otfx_engine* e, int64_t count) {
+  return e->use_tb2 ? count / 2 + count % 2 : count;
 }
 
 static void run_plain(otfx_engine* e, int64_t count) {
@@ -576,7 +631,7 @@ static void run_plain(otfx_engine* e, int64_t count) {
     CK(cudaEventRecord(e->ev_pool[slot].second, e->stream));
     e->ev_pending.emplace_back(slot, count);
   }
-  e->cur ^= int(count & 1);
+  e->cur ^= int(plain_flips(e, count) & 1);
 }
 
 // fold the timed graph launches into plain_ms once the stream has caught up
@@ -1089,6 +1144,12 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     }
     e->use_tma = plan_stages(e, std::max(3, S));
   }
+  // two-level sweep (temporal blocking), opt-in with OTFX_TB2=1: on B200 in fp64
+  // it is bound by the dependent DP chains (2x the instructions per pass at
+  // ~50 % issue), so two single sweeps are faster; see profiles/README.md
+  const bool tb2_inst = e->ops64 ? e->ops64->sweep_tb2 != nullptr : e->ops32->sweep_tb2 != nullptr;
+  e->use_tb2 = e->use_tma && tb2_inst && e->rows == n && env_int("OTFX_TB2", 0) != 0 &&
+               plan_tb2(e, env_int("OTFX_TB2_STAGES", 4));
   if (e->use_tma) {
     e->gx = (n + e->L.tile - 1) / e->L.tile;
     const int want2 = 148 * 4;
@@ -1097,6 +1158,10 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     R2 = std::max(4, std::min(128, R2));
     e->R = env_int("OTFX_TILE_ROWS", R2);
     e->gy = (e->rows + e->R - 1) / e->R;
+  }
+  if (e->use_tb2) {
+    e->gx2 = (n + e->L2.tile - 1) / e->L2.tile;
+    e->gy2 = e->gy;
   }
 
   // staging: up to 64 MB, at least two grid rows of the widest record
@@ -1140,10 +1205,18 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   e->d_stage = reinterpret_cast<double*>(e->mem + o_stage);
   if (e->use_tma) {
     for (int st = 0; st < 2; ++st) {
-      make_map(e, &e->maps[st].u, e->u[st], 2 * NP);
-      make_map(e, &e->maps[st].w, e->w[st], e->NWact);
-      make_map(e, &e->maps[st].phi, e->phi[st], NP);
-      make_map(e, &e->maps[st].diff, e->diff, NP);
+      make_map(e, &e->maps[st].u, e->u[st], 2 * NP, e->L.tw);
+      make_map(e, &e->maps[st].w, e->w[st], e->NWact, e->L.tw);
+      make_map(e, &e->maps[st].phi, e->phi[st], NP, e->L.tw);
+      make_map(e, &e->maps[st].diff, e->diff, NP, e->L.tw);
+    }
+  }
+  if (e->use_tb2) {
+    for (int st = 0; st < 2; ++st) {
+      make_map(e, &e->maps2[st].u, e->u[st], 2 * NP, e->L2.tw);
+      make_map(e, &e->maps2[st].w, e->w[st], e->NWact, e->L2.tw);
+      make_map(e, &e->maps2[st].phi, e->phi[st], NP, e->L2.tw);
+      make_map(e, &e->maps2[st].diff, e->diff, NP, e->L2.tw);
     }
   }
   CK(cudaMallocHost(&e->h_raw, 64 * sizeof(double)));
@@ -1257,6 +1330,9 @@ int otfx_engine_get_info(otfx_engine* e, otfx_engine_info* info) {
   info->regs_check = e->ops64 ? e->ops64->sweep_regs(true) : e->ops32->sweep_regs(true);
   info->graphs = e->use_graphs ? 1 : 0;
   info->tma_stages = e->use_tma ? e->L.S : 0;
+  info->tb2 = e->use_tb2 ? 1 : 0;
+  info->regs_tb2 = e->use_tb2 ? (e->ops64 ? e->ops64->tb2_regs() : e->ops32->tb2_regs()) : 0;
+  info->smem_tb2 = e->use_tb2 ? e->L2.total : 0;
   info->smem_bytes = e->use_tma ? e->L.total : int(e->smem_plain);
   if (e->use_tma) {
     info->regs_plain = e->ops64 ? e->ops64->tma_regs(false) : e->ops32->tma_regs(false);
@@ -1547,6 +1623,7 @@ int otfx_engine_attach_nccl(otfx_engine* e, const unsigned char id[128], int nra
   NK(nccl().CommInitRank(&e->comm, nranks, u, rank));
   e->nranks = nranks;
   e->rank = rank;
+  if (nranks > 1) e->use_tb2 = false;  // the two-level sweep needs depth-2 halos
   drop_graphs(e);
   API_END
 }

@@ -23,18 +23,30 @@ struct OpsFor {
       e = cudaFuncSetAttribute(tk[q], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       if (e != cudaSuccess) return e;
     }
-    return cudaFuncSetAttribute(sweep_tb2_kernel<P, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                227 * 1024);
+    if constexpr (TB2) {
+      return cudaFuncSetAttribute(sweep_tb2_kernel<P, T>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    }
+    return cudaSuccess;
   }
+  // temporal blocking is instantiated for the graph payloads with k <= 4
+  // (the matrix payloads would spill the two register-resident levels)
+  static constexpr bool TB2 = (P::NCOEF > 0 || !P::HAS_W) && P::K <= 4;
   static cudaError_t sweep_tb2(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
                                cudaStream_t s) {
-    sweep_tb2_kernel<P, T><<<g, b, a.L.total, s>>>(a, m);
-    return cudaGetLastError();
+    if constexpr (TB2) {
+      sweep_tb2_kernel<P, T><<<g, b, a.L.total, s>>>(a, m);
+      return cudaGetLastError();
+    }
+    return cudaErrorNotSupported;
   }
   static int tb2_regs() {
-    cudaFuncAttributes at;
-    cudaFuncGetAttributes(&at, sweep_tb2_kernel<P, T>);
-    return at.numRegs;
+    if constexpr (TB2) {
+      cudaFuncAttributes at;
+      cudaFuncGetAttributes(&at, sweep_tb2_kernel<P, T>);
+      return at.numRegs;
+    }
+    return 0;
   }
   static cudaError_t sweep_tma(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
                                cudaStream_t s, int fl) {
@@ -77,7 +89,7 @@ struct OpsFor {
   static const Ops<T>* table(int kind) {
     static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
                              P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &sweep_tma,
-                             &sweep_tb2, &regs, &tma_regs, &tb2_regs};
+                             TB2 ? &sweep_tb2 : nullptr, &regs, &tma_regs, &tb2_regs};
     return &o;
   }
 };
