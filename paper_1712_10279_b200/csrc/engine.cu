@@ -1124,7 +1124,10 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   const int want = 148 * 4;
   int gy = (want + e->gx - 1) / e->gx;
   int R = (e->rows + gy - 1) / gy;
-  R = std::max(4, std::min(64, R));
+  // small slabs are latency-bound (one CTA walks R rows in sequence): spread
+  // them over ~4 CTAs per SM with as few rows per CTA as possible
+  const bool small = int64_t(n) * e->rows <= int64_t(512) * 512;
+  R = small ? std::max(1, std::min(64, R)) : std::max(4, std::min(64, R));
   R = env_int("OTFX_TILE_ROWS", R);
   e->R = R;
   e->gy = (e->rows + R - 1) / R;
@@ -1134,7 +1137,9 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   e->ex = (n + 127) / 128;
   e->ey = std::min(e->rows, std::max(1, 2048 / e->ex));
   // TMA-streamed sweep: ring depth 4 (3 if that keeps two CTAs per SM)
-  e->use_tma = env_int("OTFX_TMA", 1) != 0;
+  // the TMA ring pays off once rows are long enough to pipeline; small slabs
+  // run the register-streamed sweep (measured: 4.4 vs 8.9 us/iteration at 64^2)
+  e->use_tma = env_int("OTFX_TMA", small ? 0 : 1) != 0;
   if (e->use_tma) {
     int S = env_int("OTFX_STAGES", 0);
     if (S <= 0) {

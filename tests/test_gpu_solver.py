@@ -319,6 +319,7 @@ def test_fused_check_matches_evaluate_kernel(monkeypatch, kind):
         cfg = pk.SolverConfig(tau=30.0, norm_u="l1nuc", norm_w="l1nuc", max_iters=3000)
         n, path = 24, None
     outs = []
+    monkeypatch.setenv("OTFX_TMA", "1")  # the fused check runs on the TMA sweep
     for fused in ("1", "0"):
         monkeypatch.setenv("OTFX_FUSED_CHECK", fused)
         eng = build_engine(kind, n, cfg, **args)
@@ -410,6 +411,7 @@ def test_two_level_sweep_identical(monkeypatch, n, precision):
     cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", alpha=0.05, tol_gap=1e-300,
                           tol_feas=1e-300, max_iters=157, check_every=50)
     outs = []
+    monkeypatch.setenv("OTFX_TMA", "1")  # the two-level sweep rides on the TMA plan
     for tb2 in ("1", "0"):  # opt-in path vs default path
         monkeypatch.setenv("OTFX_TB2", tb2)
         eng = build_engine("vector", n, cfg, graph=gph, precision=precision)
