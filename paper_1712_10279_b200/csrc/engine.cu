@@ -47,16 +47,16 @@ static void require(bool ok, int code, const std::string& msg) {
 }
 
 template <>
-const Ops<double>* find_ops<double>(int kind, int K) {
+const Ops<double>* find_ops<double>(int kind, int K, int ell) {
   if (kind == KIND_SCALAR) return ops_vector_f64(1, false);
   if (kind == KIND_VECTOR) return ops_vector_f64(K, true);
-  return ops_matrix_f64(kind, K);
+  return ops_matrix_f64(kind, K, ell);
 }
 template <>
-const Ops<float>* find_ops<float>(int kind, int K) {
+const Ops<float>* find_ops<float>(int kind, int K, int ell) {
   if (kind == KIND_SCALAR) return ops_vector_f32(1, false);
   if (kind == KIND_VECTOR) return ops_vector_f32(K, true);
-  return ops_matrix_f32(kind, K);
+  return ops_matrix_f32(kind, K, ell);
 }
 
 // ---------------------------------------------------------------------------
@@ -1063,8 +1063,8 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
           "unknown norm family");
   e->elem = d->dtype == OTFX_F64 ? 8 : 4;
   e->K = kind == OTFX_KIND_SCALAR ? 1 : d->k;
-  if (d->dtype == OTFX_F64) e->ops64 = find_ops<double>(kind, e->K);
-  else e->ops32 = find_ops<float>(kind, e->K);
+  if (d->dtype == OTFX_F64) e->ops64 = find_ops<double>(kind, e->K, d->ell);
+  else e->ops32 = find_ops<float>(kind, e->K, d->ell);
   const bool found = e->ops64 || e->ops32;
   require(found, OTFX_EUNSUPPORTED,
           "no sm_100a instantiation for kind=" + std::to_string(kind) + " k=" + std::to_string(e->K));

@@ -1,21 +1,20 @@
-// Instantiations: real-symmetric and complex-Hermitian matrix payloads, float.
-#include "instantiate.cuh"
+// Dispatch of the matrix payload instantiations (float); one unit per k keeps
+// the build parallel.
+#include "ops.h"
 
 namespace otfx {
 
-const Ops<float>* ops_matrix_f32(int kind, int K) {
-  if (kind == KIND_MATRIX_REAL) {
-    switch (K) {
-      case 2: return OpsFor<SymPolicy<float, 2>, float>::table(kind);
-      case 3: return OpsFor<SymPolicy<float, 3>, float>::table(kind);
-      case 4: return OpsFor<SymPolicy<float, 4>, float>::table(kind);
-      default: return nullptr;
-    }
-  }
+const Ops<float>* ops_matrix_f32_k2(int kind, int lmax);
+const Ops<float>* ops_matrix_f32_k3(int kind, int lmax);
+const Ops<float>* ops_matrix_f32_k4(int kind, int lmax);
+
+const Ops<float>* ops_matrix_f32(int kind, int K, int ell) {
+  const int lmax = ell <= 2 ? 2 : 4;
+  if (ell > 4) return nullptr;
   switch (K) {
-    case 2: return OpsFor<HermPolicy<float, 2>, float>::table(kind);
-    case 3: return OpsFor<HermPolicy<float, 3>, float>::table(kind);
-    case 4: return OpsFor<HermPolicy<float, 4>, float>::table(kind);
+    case 2: return ops_matrix_f32_k2(kind, lmax);
+    case 3: return ops_matrix_f32_k3(kind, lmax);
+    case 4: return ops_matrix_f32_k4(kind, lmax);
     default: return nullptr;
   }
 }

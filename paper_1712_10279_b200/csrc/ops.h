@@ -36,10 +36,10 @@ struct Ops {
 // registries, one per instantiation unit
 const Ops<double>* ops_vector_f64(int K, bool has_w);
 const Ops<float>* ops_vector_f32(int K, bool has_w);
-const Ops<double>* ops_matrix_f64(int kind, int K);
-const Ops<float>* ops_matrix_f32(int kind, int K);
+const Ops<double>* ops_matrix_f64(int kind, int K, int ell);
+const Ops<float>* ops_matrix_f32(int kind, int K, int ell);
 
 template <typename T>
-const Ops<T>* find_ops(int kind, int K);
+const Ops<T>* find_ops(int kind, int K, int ell);
 
 }  // namespace otfx

@@ -425,12 +425,12 @@ __device__ void herm_abs_eigs(const T (&hr)[K][K], const T (&hi)[K][K], double& 
 // Real-symmetric path.  phi/diff/u-direction block: NP = K(K+1)/2 reals
 // (diagonal first, then the strict upper triangle row-major); w block:
 // K(K-1)/2 reals (strict upper triangle of an antisymmetric matrix).
-template <typename T, int K_>
+template <typename T, int K_, int LM_ = 4>
 struct SymPolicy {
   static constexpr int K = K_;
   static constexpr int NP = K * (K + 1) / 2;
   static constexpr int NWS = K * (K - 1) / 2;
-  static constexpr int LMAX = 4;
+  static constexpr int LMAX = LM_;  // Lindblad-matrix capacity (2 or 4)
   static constexpr int NW = LMAX * NWS;
   static constexpr int NWA = NW;
   static constexpr bool HAS_W = true;
@@ -658,12 +658,12 @@ struct SymPolicy {
 // Complex Hermitian path.  A Hermitian block is K^2 reals: K real diagonal
 // entries, then (re, im) of the strict upper triangle row-major.  A skew
 // block is stored the same way with the diagonal holding imaginary parts.
-template <typename T, int K_>
+template <typename T, int K_, int LM_ = 4>
 struct HermPolicy {
   static constexpr int K = K_;
   static constexpr int NP = K * K;
   static constexpr int NWS = K * K;
-  static constexpr int LMAX = 4;
+  static constexpr int LMAX = LM_;  // Lindblad-matrix capacity (2 or 4)
   static constexpr int NW = LMAX * NWS;
   static constexpr int NWA = NW;
   static constexpr bool HAS_W = true;

@@ -1,19 +1,14 @@
-// Instantiations: scalar and vector payloads, double.
-#include "instantiate.cuh"
+// Dispatch of the scalar / vector payload instantiations (double).
+#include "ops.h"
 
 namespace otfx {
 
+const Ops<double>* ops_vector_f64_small(int K, bool has_w);
+const Ops<double>* ops_vector_f64_wide(int K);
+
 const Ops<double>* ops_vector_f64(int K, bool has_w) {
-  if (!has_w) return K == 1 ? OpsFor<VecPolicy<double, 1, false>, double>::table(KIND_SCALAR) : nullptr;
-  switch (K) {
-    case 2: return OpsFor<VecPolicy<double, 2, true>, double>::table(KIND_VECTOR);
-    case 3: return OpsFor<VecPolicy<double, 3, true>, double>::table(KIND_VECTOR);
-    case 4: return OpsFor<VecPolicy<double, 4, true>, double>::table(KIND_VECTOR);
-    case 5: return OpsFor<VecPolicy<double, 5, true>, double>::table(KIND_VECTOR);
-    case 6: return OpsFor<VecPolicy<double, 6, true>, double>::table(KIND_VECTOR);
-    case 8: return OpsFor<VecPolicy<double, 8, true>, double>::table(KIND_VECTOR);
-    default: return nullptr;
-  }
+  if (!has_w || K <= 3) return ops_vector_f64_small(K, has_w);
+  return ops_vector_f64_wide(K);
 }
 
 }  // namespace otfx
