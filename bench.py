@@ -285,8 +285,10 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.ref_n, args.cpu_seconds)
     secondary = None
+    mroof = None
     if rank == 0 and world == 1 and not args.no_secondary:
         secondary = secondary_configs(args, local)
+        mroof = matrix_roofline(args, local)
     if rank == 0:
         state_gb = info["state_bytes"] * 2 / 1e9
         line = {
@@ -325,6 +327,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "secondary": secondary,
+            "matrix_roofline": mroof,
             # sweeps + one reduction per check + the initial and final evaluate/reduce
             "gpu_launches": args.steps * ips + args.steps + 3,
             "clocks": clk.summary(),
@@ -406,6 +409,43 @@ def secondary_configs(args, device):
                         final_primal=hist[-1].primal, gpu_seconds=gms * 1e-3,
                         gpu_cell_updates_per_s=gpu_rate, cpu_cell_updates_per_s=cpu_rate,
                         cpu_sample_iterations=cpu_iters, speedup=gpu_rate / cpu_rate))
+    return out
+
+
+def matrix_roofline(args, device):
+    """The matrix payloads (BASELINE C4 / C3 families) at 2048^2, where HBM --
+    not launch latency -- bounds them: sweep time from the engine's events and
+    the compulsory-bytes roofline fraction, fp64."""
+    import torch
+
+    import paper_1712_10279_b200 as pk
+    from paper_1712_10279_b200 import synthetic
+    from paper_1712_10279_b200.solver import build_engine
+
+    peak, _ = peaks()
+    out = []
+    n = 2048
+    cases = [("C4 family: 3x3 real-symmetric DTI, l2/l1, 2 Lindblad", synthetic.matrix_blob_fixtures,
+              pk.default_lindblad3(), ("l2", "l1"), False, 7 * 6 + 2 * 2 * 3),
+             ("C3 family: 2x2 complex Hermitian, l1nuc/l1nuc, 2 Lindblad", synthetic.blob_pair_k2,
+              pk.lindblad_pair_k2(), ("l1nuc", "l1nuc"), True, (7 + 2 * 2) * 4)]
+    for name, gen, lind, norms, cplx, words in cases:
+        l0, l1 = gen(n)[:2]
+        cfg = pk.SolverConfig(tau=30.0, norm_u=norms[0], norm_w=norms[1])
+        s = torch.cuda.Stream()
+        eng = build_engine("matrix", n, cfg, lindblad=lind, complex_path=cplx, device=device,
+                           stream=s.cuda_stream)
+        eng.set_marginals(l0, l1)
+        eng.run(1e-300, 1e-300, 200, 100)
+        eng.timing(1)
+        eng.run(1e-300, 1e-300, 400, 100)
+        ms, iters = eng.timing(0)
+        eng.close()
+        per = ms / iters * 1e-3
+        balg = words * 8.0 * n * n
+        out.append(dict(config=name, n=n, ms_per_iteration=per * 1e3,
+                        cell_updates_per_s=n * n / per, bytes_per_cell=words * 8,
+                        achieved_gbs=balg / per / 1e9, frac=balg / per / peak))
     return out
 
 

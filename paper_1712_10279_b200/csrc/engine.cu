@@ -81,7 +81,7 @@ static NcclApi& nccl() {
   if (api.h) return api;
   const char* names[] = {"libnccl.so.2", "libnccl.so"};
   for (const char* nm : names) {
-    api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    api.h = dlopen(nm, RTLD_NOW | RTLD_LOCAL);  // reuses an already-loaded copy (torch)
     if (api.h) break;
   }
   require(api.h != nullptr, OTFX_ENCCL, "NCCL library (libnccl.so.2) not found");
