@@ -47,7 +47,8 @@ def parse():
     p.add_argument("--precision", choices=["f64", "f32"], default="f64")
     p.add_argument("--n", type=int, default=8192, help="grid side per GPU (weak scaling)")
     p.add_argument("--iters-per-step", type=int, default=100)
-    p.add_argument("--e2e-iters", type=int, default=1000)
+    # one e2e call = a 2000-iteration solve, the fixed count of BASELINE configs[0]
+    p.add_argument("--e2e-iters", type=int, default=2000)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--ref-n", type=int, default=2048, help="CPU sample grid side")
     p.add_argument("--cpu-seconds", type=float, default=15.0)

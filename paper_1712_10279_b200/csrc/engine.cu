@@ -249,10 +249,6 @@ __global__ void reduce_fused_kernel(const double* __restrict__ pc, const double*
 // ---------------------------------------------------------------------------
 constexpr int kPackBlocks = 296;
 
-struct EngineBase {
-  virtual ~EngineBase() {}
-};
-
 }  // namespace otfx
 
 struct otfx_engine {
