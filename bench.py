@@ -446,7 +446,7 @@ def matrix_roofline(args, device):
         balg = words * 8.0 * n * n
         out.append(dict(config=name, n=n, ms_per_iteration=per * 1e3,
                         cell_updates_per_s=n * n / per, bytes_per_cell=words * 8,
-                        achieved_gbs=balg / per / 1e9, frac=balg / per / peak))
+                        achieved_gbs=balg / per / 1e9, frac=balg / per / 1e9 / peak))
     return out
 
 
