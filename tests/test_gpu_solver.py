@@ -472,3 +472,25 @@ def test_local_slabs_other_payloads(kind):
         assert np.array_equal(cat, ref_arr), q
     for e in reversed(slabs):
         e.close()
+
+
+# ---------------------------------------------------------------------------
+# the NCCL code path with a single rank (the pool has one GPU): dlopen, comm
+# init, allreduce of the check scalars and masses, comm teardown; results must
+# equal the engine without a communicator
+# ---------------------------------------------------------------------------
+def test_nccl_single_rank_path():
+    from paper_1712_10279_b200 import distributed as D
+
+    n = 300
+    l0, l1 = synthetic.rgb_disk_pair(n)
+    gph = pk.triangle_graph()
+    cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", alpha=0.05, tol_gap=1e-300,
+                          tol_feas=1e-300, max_iters=250, check_every=100)
+    uid = pk.solver.nccl_unique_id()
+    assert len(uid) == 128
+    rep1, st1 = D.solve_vector_rows(l0, l1, gph, n, cfg, nranks=1, rank=0, unique_id=uid)
+    rep2, st2 = pk.solve_vector(pk.VectorDensity(l0), pk.VectorDensity(l1), gph, cfg=cfg)
+    np.testing.assert_array_equal(g.hist_array(rep1), g.hist_array(rep2))
+    np.testing.assert_array_equal(st1.phi, st2.phi)
+    np.testing.assert_array_equal(st1.w.values, st2.w.values)
