@@ -46,6 +46,11 @@ static void require(bool ok, int code, const std::string& msg) {
   if (!ok) throw Error(code, msg);
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 template <>
 const Ops<double>* find_ops<double>(int kind, int K, int ell) {
   if (kind == KIND_SCALAR) return ops_vector_f64(1, false);
@@ -424,8 +429,11 @@ static int round_up(int x, int a) { return (x + a - 1) / a * a; }
 static bool plan_stages(otfx_engine* e, int S) {
   StageLayout& L = e->L;
   require(S >= 3 && S <= 8, OTFX_EINVAL, "TMA ring depth must be in [3, 8]");
-  L.cw = 4;
-  L.tile = 31 * L.cw;  // 124: a multiple of 16 bytes' worth of columns for fp32 and fp64
+  // consumer warps per CTA: 8 (248 columns, half the halo re-reads) where the
+  // payload has a wide instantiation, else 4; OTFX_TMA_WARPS overrides
+  const int wide = e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw;
+  L.cw = env_int("OTFX_TMA_WARPS", wide) == 8 && wide == 8 ? 8 : 4;
+  L.tile = 31 * L.cw;  // a multiple of 16 bytes' worth of columns for fp32 and fp64
   L.h = 16 / e->elem;
   L.tw = L.tile + 2 * L.h;
   L.S = S;
@@ -562,10 +570,6 @@ static void exchange_nccl(otfx_engine* e) {
                          cudaMemcpyDeviceToDevice, e->stream));
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
 
 static void enqueue_plain(otfx_engine* e, int64_t count) {
   int64_t q = 0;

@@ -17,9 +17,11 @@ struct OpsFor {
     e = cudaFuncSetAttribute(sweep_kernel<P, T, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
-    const void* tk[4] = {(const void*)sweep_tma_kernel<P, T, 0>, (const void*)sweep_tma_kernel<P, T, 1>,
-                         (const void*)sweep_tma_kernel<P, T, 2>, (const void*)sweep_tma_kernel<P, T, 3>};
-    for (int q = 0; q < 4; ++q) {
+    const void* tk[8] = {(const void*)sweep_tma_kernel<P, T, 0, 4>, (const void*)sweep_tma_kernel<P, T, 1, 4>,
+                         (const void*)sweep_tma_kernel<P, T, 2, 4>, (const void*)sweep_tma_kernel<P, T, 3, 4>,
+                         (const void*)sweep_tma_kernel<P, T, 0, WIDE>, (const void*)sweep_tma_kernel<P, T, 1, WIDE>,
+                         (const void*)sweep_tma_kernel<P, T, 2, WIDE>, (const void*)sweep_tma_kernel<P, T, 3, WIDE>};
+    for (int q = 0; q < 8; ++q) {
       e = cudaFuncSetAttribute(tk[q], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       if (e != cudaSuccess) return e;
     }
@@ -48,22 +50,36 @@ struct OpsFor {
     }
     return 0;
   }
+  // wide CTAs (8 consumer warps, 248 columns) for the graph payloads; the
+  // matrix payloads keep 4 (their stages are large)
+  static constexpr int WIDE = (P::NCOEF > 0 || !P::HAS_W) ? 8 : 4;
+  template <int CW>
+  static void launch_tma(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
+                         cudaStream_t s, int fl) {
+    switch (fl & 3) {
+      case 0: sweep_tma_kernel<P, T, 0, CW><<<g, b, a.L.total, s>>>(a, m); break;
+      case 1: sweep_tma_kernel<P, T, 1, CW><<<g, b, a.L.total, s>>>(a, m); break;
+      case 2: sweep_tma_kernel<P, T, 2, CW><<<g, b, a.L.total, s>>>(a, m); break;
+      default: sweep_tma_kernel<P, T, 3, CW><<<g, b, a.L.total, s>>>(a, m); break;
+    }
+  }
   static cudaError_t sweep_tma(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
                                cudaStream_t s, int fl) {
-    switch (fl & 3) {
-      case 0: sweep_tma_kernel<P, T, 0><<<g, b, a.L.total, s>>>(a, m); break;
-      case 1: sweep_tma_kernel<P, T, 1><<<g, b, a.L.total, s>>>(a, m); break;
-      case 2: sweep_tma_kernel<P, T, 2><<<g, b, a.L.total, s>>>(a, m); break;
-      default: sweep_tma_kernel<P, T, 3><<<g, b, a.L.total, s>>>(a, m); break;
+    if (a.L.cw == 8) {
+      if (WIDE != 8) return cudaErrorNotSupported;
+      launch_tma<WIDE>(a, m, g, b, s, fl);
+    } else {
+      launch_tma<4>(a, m, g, b, s, fl);
     }
     return cudaGetLastError();
   }
   static int tma_regs(bool check) {
     cudaFuncAttributes at;
-    if (check) cudaFuncGetAttributes(&at, sweep_tma_kernel<P, T, 1>);
-    else cudaFuncGetAttributes(&at, sweep_tma_kernel<P, T, 0>);
+    if (check) cudaFuncGetAttributes(&at, sweep_tma_kernel<P, T, 1, WIDE>);
+    else cudaFuncGetAttributes(&at, sweep_tma_kernel<P, T, 0, WIDE>);
     return at.numRegs;
   }
+  static constexpr int wide_cw() { return WIDE; }
   static cudaError_t sweep(const SweepArgs<T>& a, dim3 g, dim3 b, size_t smem, cudaStream_t s,
                            bool check) {
     if (check)
@@ -89,7 +105,8 @@ struct OpsFor {
   static const Ops<T>* table(int kind) {
     static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
                              P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &sweep_tma,
-                             TB2 ? &sweep_tb2 : nullptr, &regs, &tma_regs, &tb2_regs};
+                             TB2 ? &sweep_tb2 : nullptr, &regs, &tma_regs, &tb2_regs,
+                             WIDE};
     return &o;
   }
 };

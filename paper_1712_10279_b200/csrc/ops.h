@@ -31,6 +31,7 @@ struct Ops {
   int (*sweep_regs)(bool check);
   int (*tma_regs)(bool check);
   int (*tb2_regs)();
+  int wide_cw;  // consumer warps of the wide TMA sweep instantiation (8, or 4 if none)
 };
 
 // registries, one per instantiation unit

@@ -91,10 +91,11 @@ struct HotArgs {
 };
 
 // compile-time shared-memory layout of one TMA row stage
-template <class P, typename T>
+template <class P, typename T, int CW_ = 4>
 struct StageShape {
+  static constexpr int CW = CW_;                    // consumer warps per CTA
   static constexpr int H = 16 / int(sizeof(T));     // halo columns (16 B)
-  static constexpr int TILE = 124;                  // output columns per CTA
+  static constexpr int TILE = 31 * CW;              // output columns per CTA
   static constexpr int TW = TILE + 2 * H;           // staged columns
   static constexpr int ROW = TW * int(sizeof(T));
   static constexpr int R128(int x) { return (x + 127) / 128 * 128; }
@@ -110,12 +111,12 @@ struct StageShape {
 // FL bit 1 (DUAL): the INPUT iterate is a checked one -- accumulate the dual
 //   norms of its gradients (S/solver.py:258-274), which this sweep computes
 //   anyway for the flux and channel updates.
-template <class P, typename T, int FL>
-__global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ TmaSweepArgs<T> G,
-                                                       const __grid_constant__ TmaSet M) {
+template <class P, typename T, int FL, int CWT = 4>
+__global__ void __launch_bounds__(32 * (CWT + 1)) sweep_tma_kernel(
+    const __grid_constant__ TmaSweepArgs<T> G, const __grid_constant__ TmaSet M) {
   constexpr bool CHECK = (FL & 1) != 0;
   constexpr bool DUAL = (FL & 2) != 0;
-  using SS = StageShape<P, T>;
+  using SS = StageShape<P, T, CWT>;
   constexpr int NP = P::NP;
   constexpr int NWA = P::NWA;
   constexpr int TW = SS::TW;
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(160) sweep_tma_kernel(const __grid_constant__ 
   unsigned char* stages = smem + 128;
   double* sred = reinterpret_cast<double*>(smem + L.off_red);
 
-  const int CW = L.cw;
+  constexpr int CW = CWT;
   const int S = L.S;
   const int t = threadIdx.x;
   const int warp = t >> 5, lane = t & 31;
