@@ -287,9 +287,11 @@ def run_ours(args):
         cpu = cpu_baseline(args.ref_n, args.cpu_seconds)
     secondary = None
     mroof = None
+    ns4096 = None
     if rank == 0 and world == 1 and not args.no_secondary:
         secondary = secondary_configs(args, local)
         mroof = matrix_roofline(args, local)
+        ns4096 = north_star_4096(args, local)
     if rank == 0:
         state_gb = info["state_bytes"] * 2 / 1e9
         line = {
@@ -329,6 +331,7 @@ def run_ours(args):
             "e2e": e2e,
             "secondary": secondary,
             "matrix_roofline": mroof,
+            "north_star_4096": ns4096,
             # sweeps + one reduction per check + the initial and final evaluate/reduce
             "gpu_launches": args.steps * ips + args.steps + 3,
             "clocks": clk.summary(),
@@ -447,6 +450,43 @@ def matrix_roofline(args, device):
         out.append(dict(config=name, n=n, ms_per_iteration=per * 1e3,
                         cell_updates_per_s=n * n / per, bytes_per_cell=words * 8,
                         achieved_gbs=balg / per / 1e9, frac=balg / per / 1e9 / peak))
+    return out
+
+
+def north_star_4096(args, device):
+    """BASELINE north_star target: the fused iteration on a 4096^2 3-channel
+    vector grid on one GPU, fp64 and fp32, as a fraction of HBM bandwidth
+    (sweep time from the engine's events over 500 iterations)."""
+    import torch
+
+    import paper_1712_10279_b200 as pk
+    from paper_1712_10279_b200 import synthetic
+    from paper_1712_10279_b200.solver import build_engine
+
+    peak, _ = peaks()
+    n = 4096
+    l0, l1 = synthetic.rgb_disk_pair(n)
+    out = {}
+    for prec in ("f64", "f32"):
+        cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1")
+        s = torch.cuda.Stream()
+        eng = build_engine("vector", n, cfg, graph=pk.triangle_graph(), precision=prec,
+                           device=device, stream=s.cuda_stream)
+        eng.set_marginals(l0, l1)
+        eng.run(1e-300, 1e-300, 300, 100)
+        eng.timing(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        eng.run(1e-300, 1e-300, 500, 100)
+        b.record(s)
+        torch.cuda.synchronize()
+        ms, iters = eng.timing(0)
+        eng.close()
+        per = ms / iters * 1e-3
+        balg = bytes_per_cell(prec) * n * n
+        out[prec] = dict(sweep_ms=per * 1e3, frac=balg / per / 1e9 / peak,
+                         cell_updates_per_s=n * n * 500 / (a.elapsed_time(b) * 1e-3),
+                         target_frac=0.70)
     return out
 
 
