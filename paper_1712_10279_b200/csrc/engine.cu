@@ -1157,11 +1157,29 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
                plan_tb2(e, env_int("OTFX_TB2_STAGES", 4));
   if (e->use_tma) {
     e->gx = (n + e->L.tile - 1) / e->L.tile;
-    const int want2 = 148 * 4;
-    int gy2 = (want2 + e->gx - 1) / e->gx;
-    int R2 = (e->rows + gy2 - 1) / gy2;
-    R2 = std::max(4, std::min(128, R2));
-    e->R = env_int("OTFX_TILE_ROWS", R2);
+    // Row split.  Short CTAs (16 rows) keep the set of CTAs resident at any
+    // moment on a compact band of rows, so the ~300 concurrent TMA streams hit
+    // few DRAM pages and the one-row halo re-reads hit L2; measured on B200
+    // (tools/wave_sweep.py, profiles/README.md): 8192^2 fp64 vector 93 % of
+    // the HBM peak at 119-row CTAs -> 98 % at 16, 4096^2 91 % -> 95 %, 3x3
+    // matrix 2048^2 81 % -> 92 %.  When that leaves only a few waves, rows per
+    // CTA grow just enough for the CTA count to fill integral waves (a
+    // partial last wave runs on a few SMs only).
+    CK(e->ops64 ? e->ops64->prepare() : e->ops32->prepare());
+    int dev_sms = 148;
+    CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, d->device));
+    const int per_sm = std::max(1, e->ops64 ? e->ops64->tma_occupancy(e->L.cw, e->L.total)
+                                            : e->ops32->tma_occupancy(e->L.cw, e->L.total));
+    const long slots = (long)dev_sms * per_sm;
+    const int r0 = 16;
+    int R = std::min(r0, e->rows);
+    const long ctas = (long)e->gx * ((e->rows + R - 1) / R);
+    const long waves = (ctas + slots - 1) / slots;
+    if (waves <= 8) {
+      const long gyw = std::max(1L, std::min<long>(waves * slots / e->gx, e->rows));
+      R = std::max(R, (int)((e->rows + gyw - 1) / gyw));
+    }
+    e->R = env_int("OTFX_TILE_ROWS", R);
     e->gy = (e->rows + e->R - 1) / e->R;
   }
   if (e->use_tb2) {

@@ -80,6 +80,15 @@ struct OpsFor {
     return at.numRegs;
   }
   static constexpr int wide_cw() { return WIDE; }
+  static int tma_occupancy(int cw, size_t smem) {
+    int nb = 0;
+    if (cw == 8 && WIDE == 8)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_tma_kernel<P, T, 0, WIDE>, 32 * (WIDE + 1),
+                                                    smem);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_tma_kernel<P, T, 0, 4>, 160, smem);
+    return nb;
+  }
   static cudaError_t sweep(const SweepArgs<T>& a, dim3 g, dim3 b, size_t smem, cudaStream_t s,
                            bool check) {
     if (check)
@@ -106,7 +115,7 @@ struct OpsFor {
     static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
                              P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &sweep_tma,
                              TB2 ? &sweep_tb2 : nullptr, &regs, &tma_regs, &tb2_regs,
-                             WIDE};
+                             WIDE,     &tma_occupancy};
     return &o;
   }
 };

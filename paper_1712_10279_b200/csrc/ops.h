@@ -32,6 +32,8 @@ struct Ops {
   int (*tma_regs)(bool check);
   int (*tb2_regs)();
   int wide_cw;  // consumer warps of the wide TMA sweep instantiation (8, or 4 if none)
+  // resident CTAs per SM of the plain TMA sweep at this width / shared memory
+  int (*tma_occupancy)(int cw, size_t smem);
 };
 
 // registries, one per instantiation unit
