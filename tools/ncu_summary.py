@@ -77,4 +77,6 @@ def main(rep, launches, dest):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 3 else None, sys.argv[-1])
+    if len(sys.argv) not in (3, 4) or not sys.argv[-1].endswith(".md"):
+        sys.exit("usage: ncu_summary.py REPORT.ncu-rep [LAUNCHES.csv] DEST.md")
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) == 4 else None, sys.argv[-1])
