@@ -114,6 +114,7 @@ typedef struct {
   int32_t tb2;           /* plain iterations run two per HBM pass (temporal blocking) */
   int32_t regs_tb2;      /* registers per thread of the two-level sweep */
   int32_t smem_tb2;      /* dynamic shared memory per two-level CTA */
+  int32_t cluster_ctas;  /* > 0: run()/step() execute on chip in one cluster of this many CTAs */
 } otfx_engine_info;
 
 int otfx_abi_version(void);

@@ -49,7 +49,8 @@ class EngineInfo(C.Structure):
                 ("tile_cols", C.c_int32), ("tile_rows", C.c_int32), ("grid_x", C.c_int32),
                 ("grid_y", C.c_int32), ("regs_plain", C.c_int32), ("regs_check", C.c_int32),
                 ("graphs", C.c_int32), ("tma_stages", C.c_int32), ("smem_bytes", C.c_int32),
-                ("tb2", C.c_int32), ("regs_tb2", C.c_int32), ("smem_tb2", C.c_int32)]
+                ("tb2", C.c_int32), ("regs_tb2", C.c_int32), ("smem_tb2", C.c_int32),
+                ("cluster_ctas", C.c_int32)]
 
 
 _P = C.c_void_p

@@ -313,6 +313,11 @@ struct otfx_engine {
   otfx::StageLayout L2{};
   otfx::TmaSet maps2[2];
   int gx2 = 1, gy2 = 1;
+  // on-chip cluster solve (small single-slab grids)
+  bool use_cluster = false;
+  int cl_ctas = 0, cl_threads = 0, cl_rows = 0;
+  size_t cl_smem = 0;
+  long long* d_result = nullptr;  // [4] iterations, history points, converged
   // policy dispatch
   const otfx::Ops<double>* ops64 = nullptr;
   const otfx::Ops<float>* ops32 = nullptr;
@@ -684,6 +689,37 @@ static void raw_fused_to_host(otfx_engine* e) {
                      e->stream));
   CK(cudaStreamSynchronize(e->stream));
   collect_timing(e);
+}
+
+// ---- on-chip cluster solve --------------------------------------------------
+static bool cluster_ok(const otfx_engine* e) { return e->use_cluster && e->nranks == 1; }
+
+template <typename T>
+static void launch_cluster(otfx_engine* e, const otfx_run_config* cfg, int64_t plain_iters) {
+  ClusterArgs<T> g;
+  memset(&g, 0, sizeof(g));
+  g.s = make_args<T>(e, e->cur);
+  g.tol_gap = cfg ? cfg->tol_gap : 0.0;
+  g.tol_feas = cfg ? cfg->tol_feas : 0.0;
+  g.diff_norm = e->diff_norm;
+  g.mu = e->d.mu;
+  g.nu = e->d.nu;
+  g.tau = e->d.tau;
+  g.max_iters = cfg ? cfg->max_iters : plain_iters;
+  g.check_every = cfg ? cfg->check_every : 1;
+  g.checks = cfg ? 1 : 0;
+  g.ctas = e->cl_ctas;
+  g.rows_max = e->cl_rows;
+  g.has_w = e->has_w ? 1 : 0;
+  g.hist = e->d_stage;
+  g.hist_cap = (long long)(e->stage_bytes / (6 * sizeof(double)));
+  g.result = e->d_result;
+  CK(ops_of<T>(e)->cluster_run(g, e->cl_ctas, e->cl_threads, e->cl_smem, e->stream));
+}
+
+static void launch_cluster(otfx_engine* e, const otfx_run_config* cfg, int64_t plain_iters) {
+  if (e->elem == 8) launch_cluster<double>(e, cfg, plain_iters);
+  else launch_cluster<float>(e, cfg, plain_iters);
 }
 
 // S/solver.py:242-291 scalar algebra, same operation order
@@ -1187,6 +1223,33 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     e->gy2 = e->gy;
   }
 
+  // On-chip solve: a small single-slab grid whose state fits in the shared
+  // memory of one cluster of up to 16 CTAs runs the whole run loop in one
+  // launch (cluster.cuh).  Measured on B200, vector 3-channel 64^2 fp64:
+  // see DESIGN.md section 4.
+  {
+    const bool inst = e->ops64 ? e->ops64->cluster_run != nullptr : e->ops32->cluster_run != nullptr;
+    if (inst && !e->use_tma && d->row_begin == 0 && d->row_end == n && n >= 2 &&
+        int64_t(n) * n <= int64_t(128) * 128 && env_int("OTFX_CLUSTER", 1) != 0) {
+      const int want = env_int("OTFX_CLUSTER_CTAS", 16);
+      for (int C = std::min(want, n); C >= 2 && !e->use_cluster; C /= 2) {
+        const int rmax = (n + C - 1) / C;
+        // one thread per cell of the band plus one per cell of the halo row
+        const int thr = (rmax * n + n + 31) / 32 * 32;
+        const size_t sm = e->ops64 ? e->ops64->cluster_smem(rmax, n) : e->ops32->cluster_smem(rmax, n);
+        if (thr > kClusterThreads || sm > 227 * 1024) break;  // fewer CTAs: taller bands
+        const int fits = e->ops64 ? e->ops64->cluster_fits(C, thr, sm) : e->ops32->cluster_fits(C, thr, sm);
+        if (fits) {
+          e->use_cluster = true;
+          e->cl_ctas = C;
+          e->cl_threads = thr;
+          e->cl_rows = rmax;
+          e->cl_smem = sm;
+        }
+      }
+    }
+  }
+
   // staging: up to 64 MB, at least two grid rows of the widest record
   const int max_rec = std::max(2 * e->K * e->K * std::max(1, d->ell) * 2, 16);
   e->stage_bytes = std::max<size_t>(size_t(128) << 20, size_t(4) * n * max_rec * sizeof(double));
@@ -1207,6 +1270,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   const size_t o_raw = carve(64 * 8);
   const size_t o_pack = carve(kPackBlocks * 3 * 8);
   const size_t o_halo = carve(halo);
+  const size_t o_result = carve(4 * sizeof(long long));
   const size_t o_stage = carve(e->stage_bytes);
   e->total_bytes = off;
   CK(cudaMalloc(&e->mem, off));
@@ -1225,6 +1289,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   e->d_raw = reinterpret_cast<double*>(e->mem + o_raw);
   e->d_pack_part = reinterpret_cast<double*>(e->mem + o_pack);
   e->d_halo = e->mem + o_halo;
+  e->d_result = reinterpret_cast<long long*>(e->mem + o_result);
   e->d_stage = reinterpret_cast<double*>(e->mem + o_stage);
   if (e->use_tma) {
     for (int st = 0; st < 2; ++st) {
@@ -1357,6 +1422,7 @@ int otfx_engine_get_info(otfx_engine* e, otfx_engine_info* info) {
   info->regs_tb2 = e->use_tb2 ? (e->ops64 ? e->ops64->tb2_regs() : e->ops32->tb2_regs()) : 0;
   info->smem_tb2 = e->use_tb2 ? e->L2.total : 0;
   info->smem_bytes = e->use_tma ? e->L.total : int(e->smem_plain);
+  info->cluster_ctas = cluster_ok(e) ? e->cl_ctas : 0;
   if (e->use_tma) {
     info->regs_plain = e->ops64 ? e->ops64->tma_regs(false) : e->ops32->tma_regs(false);
     info->regs_check = e->ops64 ? e->ops64->tma_regs(true) : e->ops32->tma_regs(true);
@@ -1450,7 +1516,8 @@ int otfx_engine_step(otfx_engine* e, int64_t iters) {
   require(e, OTFX_EINVAL, "null engine");
   require(iters >= 0, OTFX_EINVAL, "negative iteration count");
   CK(cudaSetDevice(e->d.device));
-  run_plain(e, iters);
+  if (cluster_ok(e) && iters > 0 && iters < (int64_t(1) << 30)) launch_cluster(e, nullptr, iters);
+  else run_plain(e, iters);
   e->residual_valid = false;
   API_END
 }
@@ -1512,6 +1579,29 @@ int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_poi
           "max_iters and check_every must be >= 1");
   CK(cudaSetDevice(e->d.device));
   const auto t0 = std::chrono::steady_clock::now();
+  if (cluster_ok(e) && cfg->check_every < (int64_t(1) << 30) &&
+      cfg->max_iters / cfg->check_every + 2 <=
+                           int64_t(e->stage_bytes / (6 * sizeof(double)))) {
+    // the whole run loop on the device, one launch
+    launch_cluster(e, cfg, 0);
+    long long res[4];
+    CK(cudaMemcpyAsync(res, e->d_result, sizeof(res), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    require(res[1] >= 1 && res[1] <= capacity, OTFX_EINVAL, "history buffer too small");
+    std::vector<double> h(size_t(res[1]) * 6);
+    CK(cudaMemcpyAsync(h.data(), e->d_stage, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                       e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    for (long long q = 0; q < res[1]; ++q)
+      hist[q] = {h[q * 6], h[q * 6 + 1], h[q * 6 + 2], h[q * 6 + 3], h[q * 6 + 4], h[q * 6 + 5]};
+    *n_history = res[1];
+    *iterations = res[0];
+    *converged = int(res[2]);
+    e->residual_valid = false;
+    if (wall_seconds)
+      *wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return OTFX_OK;
+  }
   int64_t nh = 0;
   auto push = [&](int64_t it, const double* r, double rk) {
     require(nh < capacity, OTFX_EINVAL, "history buffer too small");

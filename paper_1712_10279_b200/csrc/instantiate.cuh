@@ -97,6 +97,57 @@ struct OpsFor {
       sweep_kernel<P, T, false><<<g, b, smem, s>>>(a);
     return cudaGetLastError();
   }
+  // the on-chip cluster solve is instantiated for the graph / scalar payloads
+  static constexpr bool CLUSTER = (P::NCOEF > 0 || !P::HAS_W);
+  static cudaLaunchConfig_t cluster_cfg(int ctas, int threads, size_t smem, cudaStream_t s,
+                                        cudaLaunchAttribute* at) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ctas;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cfg;
+  }
+  static cudaError_t cluster_prepare() {
+    if constexpr (CLUSTER) {
+      cudaError_t e = cudaFuncSetAttribute(cluster_run_kernel<P, T>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      return cudaFuncSetAttribute(cluster_run_kernel<P, T>,
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
+    return cudaSuccess;
+  }
+  static cudaError_t cluster_run(const ClusterArgs<T>& a, int ctas, int threads, size_t smem,
+                                 cudaStream_t s) {
+    if constexpr (CLUSTER) {
+      cudaLaunchAttribute at[1];
+      cudaLaunchConfig_t cfg = cluster_cfg(ctas, threads, smem, s, at);
+      return cudaLaunchKernelEx(&cfg, cluster_run_kernel<P, T>, a);
+    }
+    return cudaErrorNotSupported;
+  }
+  static size_t cluster_smem(int rows_max, int n) { return cluster_smem_bytes<P, T>(rows_max, n); }
+  static int cluster_fits(int ctas, int threads, size_t smem) {
+    if constexpr (CLUSTER) {
+      if (cluster_prepare() != cudaSuccess) return 0;
+      cudaLaunchAttribute at[1];
+      cudaLaunchConfig_t cfg = cluster_cfg(ctas, threads, smem, nullptr, at);
+      int num = 0;
+      if (cudaOccupancyMaxActiveClusters(&num, cluster_run_kernel<P, T>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+      }
+      return num > 0 ? 1 : 0;
+    }
+    return 0;
+  }
   static cudaError_t evaluate(const SweepArgs<T>& a, dim3 g, dim3 b, cudaStream_t s) {
     evaluate_kernel<P, T><<<g, b, 0, s>>>(a);
     return cudaGetLastError();
@@ -115,7 +166,8 @@ struct OpsFor {
     static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
                              P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &sweep_tma,
                              TB2 ? &sweep_tb2 : nullptr, &regs, &tma_regs, &tb2_regs,
-                             WIDE,     &tma_occupancy};
+                             WIDE,     &tma_occupancy,
+                             CLUSTER ? &cluster_run : nullptr, &cluster_smem, &cluster_fits};
     return &o;
   }
 };

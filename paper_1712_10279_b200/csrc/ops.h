@@ -6,6 +6,7 @@
 #include "common.cuh"
 #include "sweep_tma.cuh"
 #include "sweep_tb2.cuh"
+#include "cluster.cuh"
 
 namespace otfx {
 
@@ -34,6 +35,12 @@ struct Ops {
   int wide_cw;  // consumer warps of the wide TMA sweep instantiation (8, or 4 if none)
   // resident CTAs per SM of the plain TMA sweep at this width / shared memory
   int (*tma_occupancy)(int cw, size_t smem);
+  // on-chip solve of small grids in one thread-block cluster (graph / scalar
+  // payloads; nullptr for the matrix payloads)
+  cudaError_t (*cluster_run)(const ClusterArgs<T>& a, int ctas, int threads, size_t smem,
+                             cudaStream_t s);
+  size_t (*cluster_smem)(int rows_max, int n);
+  int (*cluster_fits)(int ctas, int threads, size_t smem);  // 1 if such a cluster can launch
 };
 
 // registries, one per instantiation unit

@@ -19,12 +19,14 @@ pytestmark = pytest.mark.gpu
 F64_RTOL = 1e-10
 
 
-@pytest.mark.parametrize("sweep", ["tma", "register"])
+@pytest.mark.parametrize("sweep", ["tma", "register", "cluster"])
 @pytest.mark.parametrize("name", gu.full_cases())
 def test_golden_full_fp64(name, sweep, monkeypatch):
-    """Both sweep implementations (the small fixtures default to the register
-    sweep; the TMA-streamed one is forced here too)."""
+    """Every iteration path against the reference's own iterates: the on-chip
+    cluster solve (default for the small vector / scalar fixtures), the
+    register-streamed sweep, and the TMA-streamed sweep."""
     monkeypatch.setenv("OTFX_TMA", "1" if sweep == "tma" else "0")
+    monkeypatch.setenv("OTFX_CLUSTER", "1" if sweep == "cluster" else "0")
     meta, arrs = gu.load(name)
     rep, st = g.solve_case(meta, arrs["l0"], arrs["l1"], arrs.get("lindblad"))
     assert rep.iterations == meta["iterations"]

@@ -518,3 +518,66 @@ def test_tma_cta_widths_identical(monkeypatch, warps):
         eng.close()
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
+
+
+
+# ---------------------------------------------------------------------------
+# on-chip cluster solve (small grids: whole run loop in one cluster launch)
+# against the streamed per-iteration path: same iterates bit for bit, same
+# history up to the reduction order of the check scalars, same stopping point
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n,k,norm_u,norm_w,alpha,eps,precision,tol,iters", [
+    (64, 3, "l12", "l1", 0.3, 0.0, "f64", 1e-300, 2000),   # BASELINE C1 shape, w active
+    (37, 3, "l2", "l2", 0.05, 0.01, "f64", 1e-300, 333),
+    (60, 3, "l1", "l1", 0.05, 0.0, "f64", 1e-300, 250),
+    (32, 3, "l12", "l1", 1.0, 0.0, "f64", None, 200000),   # converges: early stop on device
+    (50, 4, "l12", "l2", 0.05, 0.0, "f32", 1e-300, 300),
+    (5, 2, "l12", "l1", 0.05, 0.0, "f64", 1e-300, 120),
+    (1, 1, "l2", "l1", 1.0, 0.0, "f64", 1e-300, 150),      # scalar (n=33)
+])
+def test_cluster_solve_matches_streamed_path(monkeypatch, n, k, norm_u, norm_w, alpha, eps,
+                                             precision, tol, iters):
+    rng = np.random.default_rng(11)
+    if k == 1:
+        n = 33
+        l0 = _norm_rand(rng, (n, n)); l1 = _norm_rand(rng, (n, n))
+        kind, args = "scalar", {}
+    elif k == 3 and n in (64, 32, 60):
+        l0, l1 = synthetic.rgb_disk_pair(n)
+        kind, args = "vector", dict(graph=pk.triangle_graph((1.0, 1.3, 0.8)))
+    else:
+        l0 = _norm_rand(rng, (n, n, k)); l1 = _norm_rand(rng, (n, n, k))
+        edges = [(a, b) for a in range(k) for b in range(a + 1, k)]
+        kind, args = "vector", dict(graph=pk.TransportGraph(k, edges, [1.0 + 0.1 * q for q in range(len(edges))]))
+    kw = dict(tau=6.0, norm_u=norm_u, norm_w=norm_w, alpha=alpha, eps_reg=eps, max_iters=iters,
+              check_every=100)
+    if tol is not None:
+        kw.update(tol_gap=tol, tol_feas=tol)
+    cfg = pk.SolverConfig(**kw)
+    outs = []
+    for cl in ("1", "0"):
+        monkeypatch.setenv("OTFX_CLUSTER", cl)
+        eng = build_engine(kind, n, cfg, precision=precision, **args)
+        assert (eng.info()["cluster_ctas"] > 0) == (cl == "1")
+        eng.set_marginals(l0, l1)
+        hist, it, conv, _ = eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+        st = eng.get_state()
+        eng.step(7)  # plain iterations after the run, through the same path
+        outs.append((g.hist_array(pk.SolveReport(conv, it, 0.0, hist)), it, conv, st,
+                     eng.get_state()))
+        eng.close()
+    (h1, it1, c1, s1, t1), (h2, it2, c2, s2, t2) = outs
+    assert it1 == it2 and c1 == c2
+    if tol is None:
+        assert c1 and it1 < iters
+    g.hist_close(h1, h2, 1e-12)
+    for a, b in zip(s1 + t1, s2 + t2):
+        if a is not None:
+            np.testing.assert_array_equal(a, b)
+
+
+def test_cluster_solve_is_default_for_small_grids():
+    for n, want in ((48, True), (64, True), (128, False), (1024, False)):
+        eng = build_engine("vector", n, pk.SolverConfig(), graph=pk.triangle_graph())
+        assert (eng.info()["cluster_ctas"] > 0) == want, n
+        eng.close()

@@ -12,7 +12,7 @@ import paper_1712_10279_b200 as pk
 from paper_1712_10279_b200 import synthetic
 from paper_1712_10279_b200.solver import build_engine
 out = {}
-for n, iters in ((64, 2000), (128, 4000), (256, 4000), (512, 2000)):
+for n, iters in ((48, 2000), (64, 2000), (80, 2000), (128, 2000)):
     l0, l1 = synthetic.rgb_disk_pair(n)
     cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", tol_gap=1e-300, tol_feas=1e-300,
                           max_iters=iters, check_every=100)
@@ -24,13 +24,11 @@ for n, iters in ((64, 2000), (128, 4000), (256, 4000), (512, 2000)):
     a.record(s); eng.run(1e-300, 1e-300, iters, 100); b.record(s); torch.cuda.synchronize()
     inf = eng.info()
     out[n] = dict(us_per_iter=1e3 * a.elapsed_time(b) / iters, tile=[inf["tile_cols"], inf["tile_rows"]],
-                  grid=[inf["grid_x"], inf["grid_y"]])
+                  grid=[inf["grid_x"], inf["grid_y"]], cluster=inf["cluster_ctas"])
     eng.close()
 print(json.dumps(out))
 '''
-for env in [{}, {"OTFX_TMA": "0"}, {"OTFX_TILE_ROWS": "1"}, {"OTFX_TILE_ROWS": "2"},
-            {"OTFX_TMA": "0", "OTFX_TILE_ROWS": "1"}, {"OTFX_TMA": "0", "OTFX_TILE_ROWS": "2"},
-            {"OTFX_TILE_ROWS": "8"}]:
+for env in [{}, {"OTFX_CLUSTER_CTAS": "8"}, {"OTFX_CLUSTER": "0"}]:
     e = dict(os.environ)
     e.update(env)
     r = subprocess.run([sys.executable, "-c", SNIP], env=e, capture_output=True, text=True,
