@@ -120,6 +120,11 @@ typedef struct {
 int otfx_abi_version(void);
 const char* otfx_last_error(void);
 int otfx_device_count(int* count);
+/* Engine memory comes from a per-device stream-ordered pool that keeps freed
+ * blocks cached for the next engine (no reference counterpart: NumPy's
+ * allocator plays this role in S/solver.py:179-201).  Returns the cached
+ * blocks of every device to the driver. */
+int otfx_release_cached_memory(void);
 
 int otfx_engine_create(const otfx_engine_desc* desc, otfx_engine** out);
 int otfx_engine_destroy(otfx_engine* e);

@@ -16,4 +16,6 @@ from .solver import (CudaEngine, HistoryPoint, NormFamily, SolveReport, SolverCo
                      default_tau, duality_gap, residual_Rk, solve_matrix, solve_scalar,
                      solve_vector, step_sizes_matrix, step_sizes_scalar, step_sizes_vector)
 
+from ._lib import release_cached_memory
+
 __version__ = "0.1.0"

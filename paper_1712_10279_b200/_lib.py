@@ -59,6 +59,7 @@ SIGNATURES = {
     "otfx_abi_version": (C.c_int, []),
     "otfx_last_error": (C.c_char_p, []),
     "otfx_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "otfx_release_cached_memory": (C.c_int, []),
     "otfx_engine_create": (C.c_int, [C.POINTER(EngineDesc), C.POINTER(_P)]),
     "otfx_engine_destroy": (C.c_int, [_P]),
     "otfx_engine_get_info": (C.c_int, [_P, C.POINTER(EngineInfo)]),
@@ -116,6 +117,11 @@ def check(rc: int):
     if rc == EUNSUPPORTED:
         raise UnsupportedNormError(msg)
     raise NumericalError(f"otfx error {rc}: {msg}")
+
+
+def release_cached_memory() -> None:
+    """Give the engine memory pool's cached blocks back to the driver."""
+    check(load().otfx_release_cached_memory())
 
 
 def device_count() -> int:

@@ -266,6 +266,7 @@ struct otfx_engine {
   int64_t plane = 0;
   size_t state_bytes = 0, total_bytes = 0;
   unsigned char* mem = nullptr;
+  bool pooled = false;  // mem came from the library's device pool
   void* u[2]{};
   void* w[2]{};
   void* phi[2]{};
@@ -689,6 +690,26 @@ static void raw_fused_to_host(otfx_engine* e) {
                      e->stream));
   CK(cudaStreamSynchronize(e->stream));
   collect_timing(e);
+}
+
+// ---- device memory pool ------------------------------------------------------
+static std::mutex g_pool_mu;
+static std::map<int, cudaMemPool_t> g_pools;
+
+static cudaMemPool_t device_pool(int device) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto it = g_pools.find(device);
+  if (it != g_pools.end()) return it->second;
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  cudaMemPool_t pool;
+  CK(cudaMemPoolCreate(&pool, &props));
+  uint64_t keep = UINT64_MAX;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  g_pools.emplace(device, pool);
+  return pool;
 }
 
 // ---- on-chip cluster solve --------------------------------------------------
@@ -1273,7 +1294,17 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   const size_t o_result = carve(4 * sizeof(long long));
   const size_t o_stage = carve(e->stage_bytes);
   e->total_bytes = off;
-  CK(cudaMalloc(&e->mem, off));
+  // stream-ordered allocation from the library's per-device pool: freed
+  // blocks stay cached (release threshold = max), so a solve that follows
+  // another one of the same size skips cudaMalloc / cudaFree (hundreds of ms
+  // at 8192^2); otfx_release_cached_memory() trims the pool
+  if (env_int("OTFX_POOL", 1) != 0) {
+    CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&e->mem), off, device_pool(d->device),
+                               e->stream));
+    e->pooled = true;
+  } else {
+    CK(cudaMalloc(&e->mem, off));
+  }
   CK(cudaMemsetAsync(e->mem, 0, o_stage, e->stream));
   for (int s = 0; s < 2; ++s) {
     unsigned char* b = e->mem + (s ? o_state1 : o_state0);
@@ -1323,7 +1354,14 @@ static void destroy(otfx_engine* e) {
   }
   if (e->stream) cudaStreamSynchronize(e->stream);
   if (e->comm && nccl().CommDestroy) nccl().CommDestroy(e->comm);
-  if (e->mem) cudaFree(e->mem);
+  if (e->mem) {
+    if (e->pooled) {
+      cudaFreeAsync(e->mem, e->stream);
+      cudaStreamSynchronize(e->stream);  // the block is reusable from any stream
+    } else {
+      cudaFree(e->mem);
+    }
+  }
   if (e->h_raw) cudaFreeHost(e->h_raw);
   if (e->h_pack_part) cudaFreeHost(e->h_pack_part);
   if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
@@ -1363,6 +1401,17 @@ extern "C" {
 int otfx_abi_version(void) { return OTFX_ABI_VERSION; }
 
 const char* otfx_last_error(void) { return g_err.c_str(); }
+
+int otfx_release_cached_memory(void) {
+  API_BEGIN
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (auto& pr : g_pools) {
+    CK(cudaSetDevice(pr.first));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemPoolTrimTo(pr.second, 0));
+  }
+  API_END
+}
 
 int otfx_device_count(int* count) {
   API_BEGIN

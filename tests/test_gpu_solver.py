@@ -581,3 +581,20 @@ def test_cluster_solve_is_default_for_small_grids():
         eng = build_engine("vector", n, pk.SolverConfig(), graph=pk.triangle_graph())
         assert (eng.info()["cluster_ctas"] > 0) == want, n
         eng.close()
+
+
+def test_pooled_engines_reuse_memory_and_release():
+    """Engine memory comes from the library's stream-ordered pool: a second
+    engine of the same size reuses the cached block (no stale state: the
+    iterate starts from zero), and the cache can be trimmed."""
+    l0, l1 = synthetic.rgb_disk_pair(300)
+    cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", tol_gap=1e-300, tol_feas=1e-300,
+                          max_iters=50, check_every=25)
+    states = []
+    for _ in range(2):
+        rep, st = pk.solve_vector(pk.VectorDensity(l0), pk.VectorDensity(l1), pk.triangle_graph(),
+                                  cfg=cfg)
+        states.append((rep.transport_value, st.phi))
+    assert states[0][0] == states[1][0]
+    np.testing.assert_array_equal(states[0][1], states[1][1])
+    pk.release_cached_memory()
