@@ -166,6 +166,13 @@ int otfx_engine_step_check(otfx_engine* e, double out[5]);
 int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_point* history,
                     int64_t capacity, int64_t* n_history, int64_t* iterations, int* converged,
                     double* wall_seconds);
+/* the same run loop over the row slabs of one grid held by `count` engines on
+ * one device and one stream (in row order, diff norms already combined),
+ * stepped in lockstep with local halo copies: the single-GPU stand-in for the
+ * NCCL-connected ranks (same check cadence, fused checks and stopping rule) */
+int otfx_engines_run_local(otfx_engine* const* engines, int count, const otfx_run_config* cfg,
+                           otfx_history_point* history, int64_t capacity, int64_t* n_history,
+                           int64_t* iterations, int* converged);
 
 /* fixed-point residual between two given iterates (residual_Rk,
  * S/solver.py:501-526), using the engine's mu, nu, tau; whole-grid engines */

@@ -75,6 +75,10 @@ SIGNATURES = {
     "otfx_engine_run": (C.c_int, [_P, C.POINTER(RunConfig), C.POINTER(HistoryPointC), C.c_int64,
                                   C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                   C.POINTER(C.c_int), _DP]),
+    "otfx_engines_run_local": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(RunConfig),
+                                         C.POINTER(HistoryPointC), C.c_int64,
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int)]),
     "otfx_engine_residual_between": (C.c_int, [_P] + [_P] * 8 + [_DP]),
     "otfx_engine_sweep": (C.c_int, [_P, C.c_int]),
     "otfx_engine_raw": (C.c_int, [_P, C.c_int, _DP]),

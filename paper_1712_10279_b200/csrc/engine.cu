@@ -1383,6 +1383,114 @@ static void zero_state(otfx_engine* e) {
 // ===========================================================================
 using namespace otfx;
 
+namespace otfx {
+
+// The engines the run loop drives: one engine (a whole grid, or this rank's
+// slab of an NCCL-connected decomposition), or the P slabs of one grid on one
+// device stepped in lockstep with local halo copies -- the single-GPU stand-in
+// for the NCCL transport, which runs the same loop (tests/test_gpu_solver.py).
+struct SlabGroup {
+  otfx_engine* const* es;
+  int count;
+  bool local() const { return count > 1; }
+  otfx_engine* lead() const { return es[0]; }
+};
+
+static void exchange_local_impl(otfx_engine* const* es, int count) {
+  for (int s = 0; s + 1 < count; ++s) {
+    otfx_engine* a = es[s];
+    otfx_engine* b = es[s + 1];
+    require(a->stream == b->stream, OTFX_EINVAL, "local exchange needs one shared stream");
+    require(a->d.row_end == b->d.row_begin && a->d.n == b->d.n && a->elem == b->elem &&
+                a->NP == b->NP && a->pitch == b->pitch,
+            OTFX_EINVAL, "engines are not adjacent slabs of one grid");
+    require(a->cur == b->cur, OTFX_EINVAL, "engines are at different iterations");
+    const int c = a->cur;
+    // a's bottom ghost <- b's first row (phi)
+    copy_rows(a, a->phi[c], a->rows + 1, b, b->phi[c], 1, a->NP, a->stream);
+    // b's top ghost <- a's last row (phi, u)
+    copy_rows(b, b->phi[c], 0, a, a->phi[c], a->rows, a->NP, a->stream);
+    copy_rows(b, b->u[c], 0, a, a->u[c], a->rows, 2 * a->NP, a->stream);
+  }
+}
+
+// one iteration of every slab, then the halo exchange
+static void group_sweep(const SlabGroup& g, int fl) {
+  for (int q = 0; q < g.count; ++q) launch_sweep(g.es[q], fl);
+  if (g.local()) exchange_local_impl(g.es, g.count);
+  else exchange_nccl(g.lead());
+}
+
+static void group_plain(const SlabGroup& g, int64_t count) {
+  if (!g.local()) {
+    run_plain(g.lead(), count);
+    return;
+  }
+  for (int64_t q = 0; q < count; ++q) group_sweep(g, 0);
+}
+
+// raw check scalars of the group: NCCL-allreduced for a rank, summed / maxed
+// over the slabs (in slab order) for a local group
+static void group_raw(const SlabGroup& g, bool fused, bool with_res, double raw[OTFX_NRAW]) {
+  for (int q = 0; q < OTFX_NRAW; ++q) raw[q] = 0.0;
+  for (int s = 0; s < g.count; ++s) {
+    otfx_engine* e = g.es[s];
+    if (fused) raw_fused_to_host(e);
+    else raw_to_host(e, with_res, !g.local());
+    for (int q = 0; q < R_NSUM; ++q) raw[q] += e->h_raw[q];
+    for (int q = R_NSUM; q < OTFX_NRAW; ++q) raw[q] = s ? std::max(raw[q], e->h_raw[q]) : e->h_raw[q];
+  }
+}
+
+// the _run loop (S/solver.py:294-337) over a slab group
+static void run_loop(const SlabGroup& g, const otfx_run_config* cfg, otfx_history_point* hist,
+                     int64_t capacity, int64_t* n_history, int64_t* iterations, int* converged) {
+  otfx_engine* e = g.lead();
+  int64_t nh = 0;
+  auto push = [&](int64_t it, const double* r, double rk) {
+    require(nh < capacity, OTFX_EINVAL, "history buffer too small");
+    hist[nh++] = {double(it), r[0], r[1], r[2], r[3], rk};
+  };
+  double r[5], raw[OTFX_NRAW];
+  group_raw(g, false, false, raw);
+  finalize(e, raw, r);
+  push(0, r, std::nan(""));
+  bool conv = r[2] <= cfg->tol_gap && r[3] <= cfg->tol_feas;
+  int64_t it = 0;
+  const int64_t ce = cfg->check_every, mx = cfg->max_iters;
+  bool fused_ok = env_int("OTFX_FUSED_CHECK", 1) != 0;
+  for (int q = 0; q < g.count; ++q) fused_ok = fused_ok && g.es[q]->use_tma;
+  while (!conv && it < mx) {
+    const int64_t next = std::min((it / ce + 1) * ce, mx);
+    group_plain(g, next - it - 1);
+    it = next - 1;
+    // Fused check: the iteration after the check runs speculatively and
+    // accumulates the dual norms of the checked iterate; it is kept when the
+    // run continues and dropped (ping-pong buffer flipped back) when it stops.
+    // It must not itself be a check iteration.
+    const bool fuse = fused_ok && next + 1 < mx && (next + 1) % ce != 0;
+    group_sweep(g, 1);
+    if (fuse) group_sweep(g, 2);
+    group_raw(g, fuse, true, raw);
+    finalize(e, raw, r);
+    it = next;
+    push(it, r, r[4]);
+    conv = r[2] <= cfg->tol_gap && r[3] <= cfg->tol_feas;
+    if (fuse) {
+      if (conv) {
+        for (int q = 0; q < g.count; ++q) g.es[q]->cur ^= 1;  // drop the speculative iterate
+      } else {
+        ++it;  // keep it: iteration next+1 is done
+      }
+    }
+  }
+  *n_history = nh;
+  *iterations = it;
+  *converged = conv ? 1 : 0;
+}
+
+}  // namespace otfx
+
 #define API_BEGIN try {
 #define API_END                        \
   }                                    \
@@ -1651,51 +1759,28 @@ int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_poi
       *wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return OTFX_OK;
   }
-  int64_t nh = 0;
-  auto push = [&](int64_t it, const double* r, double rk) {
-    require(nh < capacity, OTFX_EINVAL, "history buffer too small");
-    hist[nh++] = {double(it), r[0], r[1], r[2], r[3], rk};
-  };
-  double r[5];
-  raw_to_host(e, false, true);
-  finalize(e, e->h_raw, r);
-  push(0, r, std::nan(""));
-  bool conv = r[2] <= cfg->tol_gap && r[3] <= cfg->tol_feas;
-  int64_t it = 0;
-  const int64_t ce = cfg->check_every, mx = cfg->max_iters;
-  const bool fused_ok = e->use_tma && env_int("OTFX_FUSED_CHECK", 1) != 0;
-  while (!conv && it < mx) {
-    const int64_t next = std::min((it / ce + 1) * ce, mx);
-    run_plain(e, next - it - 1);
-    it = next - 1;
-    // Fused check: the iteration after the check runs speculatively and
-    // accumulates the dual norms of the checked iterate; it is kept when the
-    // run continues and dropped (ping-pong buffer flipped back) when it stops.
-    // It must not itself be a check iteration.
-    const bool fuse = fused_ok && next + 1 < mx && (next + 1) % ce != 0;
-    launch_sweep(e, 1);
-    exchange_nccl(e);
-    if (fuse) {
-      launch_sweep(e, 2);
-      exchange_nccl(e);
-      raw_fused_to_host(e);
-    } else {
-      raw_to_host(e, true, true);
-    }
-    finalize(e, e->h_raw, r);
-    it = next;
-    push(it, r, r[4]);
-    conv = r[2] <= cfg->tol_gap && r[3] <= cfg->tol_feas;
-    if (fuse) {
-      if (conv) e->cur ^= 1;  // drop the speculative iterate
-      else ++it;              // keep it: iteration next+1 is done
-    }
-  }
-  *n_history = nh;
-  *iterations = it;
-  *converged = conv ? 1 : 0;
+  run_loop(SlabGroup{&e, 1}, cfg, hist, capacity, n_history, iterations, converged);
   if (wall_seconds)
     *wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  API_END
+}
+
+int otfx_engines_run_local(otfx_engine* const* es, int count, const otfx_run_config* cfg,
+                           otfx_history_point* hist, int64_t capacity, int64_t* n_history,
+                           int64_t* iterations, int* converged) {
+  API_BEGIN
+  require(es && count >= 1 && cfg && hist && n_history && iterations && converged, OTFX_EINVAL,
+          "null pointer");
+  require(cfg->max_iters >= 1 && cfg->check_every >= 1, OTFX_EINVAL,
+          "max_iters and check_every must be >= 1");
+  for (int q = 0; q < count; ++q) {
+    require(es[q]->nranks == 1, OTFX_EINVAL, "local slab groups cannot carry a communicator");
+    require(es[q]->d.row_begin == (q ? es[q - 1]->d.row_end : 0) &&
+                (q + 1 < count || es[q]->d.row_end == es[q]->d.n),
+            OTFX_EINVAL, "engines must be the slabs of one grid, in order");
+  }
+  CK(cudaSetDevice(es[0]->d.device));
+  run_loop(SlabGroup{es, count}, cfg, hist, capacity, n_history, iterations, converged);
   API_END
 }
 
@@ -1746,22 +1831,8 @@ int otfx_engine_residual_between(otfx_engine* e, const double* ux0, const double
 int otfx_engine_exchange_local(otfx_engine* const* es, int count) {
   API_BEGIN
   require(es && count >= 1, OTFX_EINVAL, "no engines");
-  for (int s = 0; s + 1 < count; ++s) {
-    otfx_engine* a = es[s];
-    otfx_engine* b = es[s + 1];
-    require(a->stream == b->stream, OTFX_EINVAL, "local exchange needs one shared stream");
-    require(a->d.row_end == b->d.row_begin && a->d.n == b->d.n && a->elem == b->elem &&
-                a->NP == b->NP && a->pitch == b->pitch,
-            OTFX_EINVAL, "engines are not adjacent slabs of one grid");
-    require(a->cur == b->cur, OTFX_EINVAL, "engines are at different iterations");
-    const int c = a->cur;
-    CK(cudaSetDevice(a->d.device));
-    // a's bottom ghost <- b's first row (phi)
-    copy_rows(a, a->phi[c], a->rows + 1, b, b->phi[c], 1, a->NP, a->stream);
-    // b's top ghost <- a's last row (phi, u)
-    copy_rows(b, b->phi[c], 0, a, a->phi[c], a->rows, a->NP, a->stream);
-    copy_rows(b, b->u[c], 0, a, a->u[c], a->rows, 2 * a->NP, a->stream);
-  }
+  CK(cudaSetDevice(es[0]->d.device));
+  exchange_local_impl(es, count);
   API_END
 }
 

@@ -352,6 +352,21 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def run_local(engines, tol_gap, tol_feas, max_iters, check_every):
+    """The run loop over the row-slab engines of one grid on one device, in
+    lockstep with local halo copies (the single-GPU stand-in for NCCL ranks)."""
+    cap = max_iters // check_every + 3
+    hist = (_lib.HistoryPointC * cap)()
+    cfg = _lib.RunConfig(tol_gap, tol_feas, int(max_iters), int(check_every))
+    nh, it, conv = C.c_int64(), C.c_int64(), C.c_int()
+    arr = (C.c_void_p * len(engines))(*[e.handle for e in engines])
+    _lib.check(_lib.load().otfx_engines_run_local(arr, len(engines), C.byref(cfg), hist, cap,
+                                                  C.byref(nh), C.byref(it), C.byref(conv)))
+    history = [HistoryPoint(int(h.iteration), h.primal, h.dual, h.gap_ratio, h.feas_residual,
+                            h.residual) for h in hist[: nh.value]]
+    return history, it.value, bool(conv.value)
+
+
 def exchange_local(engines):
     arr = (C.c_void_p * len(engines))(*[e.handle for e in engines])
     _lib.check(_lib.load().otfx_engine_exchange_local(arr, len(engines)))

@@ -598,3 +598,51 @@ def test_pooled_engines_reuse_memory_and_release():
     assert states[0][0] == states[1][0]
     np.testing.assert_array_equal(states[0][1], states[1][1])
     pk.release_cached_memory()
+
+
+# ---------------------------------------------------------------------------
+# the distributed run loop (fused checks, speculative dual sweep, stopping
+# rule) over P row slabs of one grid on one GPU, with the TMA-streamed slab
+# sweeps the multi-GPU bench runs: same iterates and history as one engine
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("P,n,force_tma,conv", [
+    (2, 300, True, False), (3, 301, True, False), (2, 1100, False, False), (2, 32, True, True),
+])
+def test_local_slab_run_loop_matches_single_engine(monkeypatch, P, n, force_tma, conv):
+    from paper_1712_10279_b200.solver import run_local
+    if force_tma:
+        monkeypatch.setenv("OTFX_TMA", "1")
+    l0, l1 = synthetic.rgb_disk_pair(n)
+    gph = pk.triangle_graph((1.0, 1.2, 0.9))
+    if conv:
+        cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", alpha=1.0, max_iters=200000)
+    else:
+        cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", alpha=0.05, tol_gap=1e-300,
+                              tol_feas=1e-300, max_iters=230, check_every=50)
+    whole = build_engine("vector", n, cfg, graph=gph)
+    assert whole.info()["tma_stages"] > 0
+    whole.set_marginals(l0, l1)
+    hist1, it1, c1, _ = whole.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+    ref = whole.get_state()
+    whole.close()
+    bounds = np.linspace(0, n, P + 1).astype(int)
+    slabs, stream = [], None
+    for r in range(P):
+        e = build_engine("vector", n, cfg, graph=gph, rows=(bounds[r], bounds[r + 1]), stream=stream)
+        assert e.info()["tma_stages"] > 0
+        stream = e.stream
+        e.set_marginals(l0[bounds[r]:bounds[r + 1]], l1[bounds[r]:bounds[r + 1]])
+        slabs.append(e)
+    dn = float(np.sqrt(sum(e.diff_norm ** 2 for e in slabs)))
+    for e in slabs:
+        e.diff_norm = dn
+    hist2, it2, c2 = run_local(slabs, cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+    assert it1 == it2 and c1 == c2 == conv
+    g.hist_close(g.hist_array(pk.SolveReport(c1, it1, 0.0, hist1)),
+                 g.hist_array(pk.SolveReport(c2, it2, 0.0, hist2)), 1e-12)
+    got = [e.get_state() for e in slabs]
+    for q, ref_arr in enumerate(ref):
+        cat = np.concatenate([s[q] for s in got], axis=0)
+        assert np.array_equal(cat, ref_arr), q
+    for e in reversed(slabs):
+        e.close()
