@@ -112,7 +112,17 @@ struct StageShape {
 //   norms of its gradients (S/solver.py:258-274), which this sweep computes
 //   anyway for the flux and channel updates.
 template <class P, typename T, int FL, int CWT = 4>
-__global__ void __launch_bounds__(32 * (CWT + 1)) sweep_tma_kernel(
+//
+// Occupancy hints, measured on B200 (profiles/README.md): the wide check and
+// dual sweeps are held to two resident CTAs per SM (<= 96 registers; at their
+// natural 126-156 the check sweep ran one CTA per SM and took 2.6x a plain
+// sweep), and the plain sweep states minBlocks = 1 explicitly, which steers
+// ptxas to a 70-register schedule for fp32 (12 % faster than the 56-register
+// one it picks without the hint; fp64 unchanged).
+// The 4-warp instantiations (matrix payloads) keep ptxas' default (0 = no
+// hint): stating minBlocks = 1 there raises the 3x3 real payload from 156 to
+// 196 registers and halves its occupancy.
+__global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) : 0) sweep_tma_kernel(
     const __grid_constant__ TmaSweepArgs<T> G, const __grid_constant__ TmaSet M) {
   constexpr bool CHECK = (FL & 1) != 0;
   constexpr bool DUAL = (FL & 2) != 0;
