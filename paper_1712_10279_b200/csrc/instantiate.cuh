@@ -89,6 +89,11 @@ struct OpsFor {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_tma_kernel<P, T, 0, 4>, 160, smem);
     return nb;
   }
+  static int sweep_occupancy(int threads, size_t smem) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_kernel<P, T, false>, threads, smem);
+    return nb;
+  }
   static cudaError_t sweep(const SweepArgs<T>& a, dim3 g, dim3 b, size_t smem, cudaStream_t s,
                            bool check) {
     if (check)
@@ -166,7 +171,7 @@ struct OpsFor {
     static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
                              P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &sweep_tma,
                              TB2 ? &sweep_tb2 : nullptr, &regs, &tma_regs, &tb2_regs,
-                             WIDE,     &tma_occupancy,
+                             WIDE,     &tma_occupancy, &sweep_occupancy,
                              CLUSTER ? &cluster_run : nullptr, &cluster_smem, &cluster_fits};
     return &o;
   }

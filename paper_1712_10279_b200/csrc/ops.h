@@ -35,6 +35,8 @@ struct Ops {
   int wide_cw;  // consumer warps of the wide TMA sweep instantiation (8, or 4 if none)
   // resident CTAs per SM of the plain TMA sweep at this width / shared memory
   int (*tma_occupancy)(int cw, size_t smem);
+  // resident CTAs per SM of the plain register-streamed sweep
+  int (*sweep_occupancy)(int threads, size_t smem);
   // on-chip solve of small grids in one thread-block cluster (graph / scalar
   // payloads; nullptr for the matrix payloads)
   cudaError_t (*cluster_run)(const ClusterArgs<T>& a, int ctas, int threads, size_t smem,
