@@ -509,9 +509,13 @@ def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn):
         def call():
             return pk.solve_vector(a, b, graph, cfg=cfg, precision=args.precision, device=local)
     else:
+        # one communicator per process, reused by every solve (set up once,
+        # like the process group)
+        comm = D.SlabCommunicator(uid_fn(), world, rank, local)
+
         def call():
             return D.solve_vector_rows(l0, l1, graph, n, cfg, nranks=world, rank=rank,
-                                       unique_id=uid_fn(), precision=args.precision, device=local)
+                                       precision=args.precision, device=local, comm=comm)
     call()  # warm-up (allocations, graph capture)
     times = []
     for _ in range(args.e2e_steps):

@@ -199,6 +199,14 @@ int otfx_nccl_unique_id(unsigned char id[128]);
  * slab); the engine then exchanges halo rows after every iteration and
  * allreduces the check scalars */
 int otfx_engine_attach_nccl(otfx_engine* e, const unsigned char id[128], int nranks, int rank);
+/* a communicator that outlives engines: created once per process and rank,
+ * attached (non-owning) to every engine of a series of solves, so the NCCL
+ * setup is paid once rather than per solve */
+typedef struct otfx_comm otfx_comm;
+int otfx_comm_create(const unsigned char id[128], int nranks, int rank, int device,
+                     otfx_comm** out);
+int otfx_comm_destroy(otfx_comm* c);
+int otfx_engine_attach_comm(otfx_engine* e, otfx_comm* c);
 
 /* device time of the plain-iteration graph launches (CUDA events on the
  * engine stream): returns the time / sweep count accumulated so far, then

@@ -86,6 +86,10 @@ SIGNATURES = {
     "otfx_engine_exchange_local": (C.c_int, [C.POINTER(_P), C.c_int]),
     "otfx_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
     "otfx_engine_attach_nccl": (C.c_int, [_P, C.POINTER(C.c_ubyte), C.c_int, C.c_int]),
+    "otfx_comm_create": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_void_p)]),
+    "otfx_comm_destroy": (C.c_int, [_P]),
+    "otfx_engine_attach_comm": (C.c_int, [_P, _P]),
     "otfx_engine_timing": (C.c_int, [_P, C.c_int, _DP, C.POINTER(C.c_int64)]),
     "otfx_engine_sync": (C.c_int, [_P]),
     "otfx_engine_stream": (C.c_void_p, [_P]),

@@ -256,6 +256,11 @@ constexpr int kPackBlocks = 296;
 
 }  // namespace otfx
 
+struct otfx_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+};
+
 struct otfx_engine {
   otfx_engine_desc d{};
   std::vector<double> chan;
@@ -303,6 +308,7 @@ struct otfx_engine {
   std::map<std::pair<int, int64_t>, cudaGraphExec_t> graphs;
   // NCCL
   ncclComm_t comm = nullptr;
+  bool own_comm = false;  // created by attach_nccl (destroyed with the engine)
   int nranks = 1, rank = 0;
   void* d_halo = nullptr;  // send/recv buffers
   // TMA-streamed sweep
@@ -1382,7 +1388,7 @@ static void destroy(otfx_engine* e) {
     cudaEventDestroy(pr.second);
   }
   if (e->stream) cudaStreamSynchronize(e->stream);
-  if (e->comm && nccl().CommDestroy) nccl().CommDestroy(e->comm);
+  if (e->comm && e->own_comm && nccl().CommDestroy) nccl().CommDestroy(e->comm);
   if (e->mem) {
     if (e->pooled) {
       cudaFreeAsync(e->mem, e->stream);
@@ -1882,10 +1888,57 @@ int otfx_engine_attach_nccl(otfx_engine* e, const unsigned char id[128], int nra
   CK(cudaSetDevice(e->d.device));
   ncclUniqueId u;
   memcpy(&u, id, 128);
+  require(!e->comm, OTFX_EINVAL, "engine already has a communicator");
   NK(nccl().CommInitRank(&e->comm, nranks, u, rank));
+  e->own_comm = true;
   e->nranks = nranks;
   e->rank = rank;
   if (nranks > 1) e->use_tb2 = false;  // the two-level sweep needs depth-2 halos
+  drop_graphs(e);
+  API_END
+}
+
+int otfx_comm_create(const unsigned char id[128], int nranks, int rank, int device,
+                     otfx_comm** out) {
+  API_BEGIN
+  require(id && out, OTFX_EINVAL, "null pointer");
+  require(nranks >= 1 && rank >= 0 && rank < nranks, OTFX_EINVAL, "bad rank");
+  CK(cudaSetDevice(device));
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  auto* c = new otfx_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  try {
+    NK(nccl().CommInitRank(&c->comm, nranks, u, rank));
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  *out = c;
+  API_END
+}
+
+int otfx_comm_destroy(otfx_comm* c) {
+  API_BEGIN
+  if (c) {
+    if (c->comm && nccl().CommDestroy) nccl().CommDestroy(c->comm);
+    delete c;
+  }
+  API_END
+}
+
+int otfx_engine_attach_comm(otfx_engine* e, otfx_comm* c) {
+  API_BEGIN
+  require(e && c, OTFX_EINVAL, "null pointer");
+  require(!e->comm, OTFX_EINVAL, "engine already has a communicator");
+  require(c->device == e->d.device, OTFX_EINVAL, "communicator and engine on different devices");
+  e->comm = c->comm;
+  e->own_comm = false;
+  e->nranks = c->nranks;
+  e->rank = c->rank;
+  if (c->nranks > 1) e->use_tb2 = false;
   drop_graphs(e);
   API_END
 }

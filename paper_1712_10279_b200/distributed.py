@@ -17,6 +17,9 @@ from __future__ import annotations
 
 import numpy as np
 
+import ctypes as C
+
+from . import _lib
 from .solver import (SolverConfig, _mass_check, _pack_state, SolveReport, build_engine,
                      nccl_unique_id, validate_norm)
 
@@ -54,25 +57,55 @@ def share_unique_id(dist, rank):
     return obj[0]
 
 
-def make_vector_slab_engine(n, graph, cfg: SolverConfig, *, nranks, rank, unique_id,
-                            precision="f64", device=0, stream=None):
+class SlabCommunicator:
+    """An NCCL communicator for this rank's slab that outlives the engines of a
+    series of solves (the NCCL setup is paid once, not per solve)."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int, device: int = 0):
+        buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        _lib.check(_lib.load().otfx_comm_create(buf, nranks, rank, device, C.byref(h)))
+        self.handle = h
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    def close(self):
+        if self.handle:
+            _lib.check(_lib.load().otfx_comm_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_vector_slab_engine(n, graph, cfg: SolverConfig, *, nranks, rank, unique_id=None,
+                            precision="f64", device=0, stream=None, comm=None):
     validate_norm(cfg.norm_u, "vector", "u")
     validate_norm(cfg.norm_w, "vector", "w")
     b = slab_bounds(n, nranks)
     eng = build_engine("vector", n, cfg, graph=graph, precision=precision, device=device,
                        rows=(b[rank], b[rank + 1]), stream=stream)
-    if nranks > 1:
+    if comm is not None:
+        if (comm.nranks, comm.rank) != (nranks, rank):
+            eng.close()
+            raise ValueError("communicator was created for another rank layout")
+        eng.attach_comm(comm)
+    elif nranks > 1:
         eng.attach_nccl(unique_id, nranks, rank)
     return eng
 
 
 def solve_vector_rows(l0_rows, l1_rows, graph, n, cfg: SolverConfig | None = None, *, nranks,
-                      rank, unique_id, precision="f64", device=0):
+                      rank, unique_id=None, precision="f64", device=0, comm=None):
     """Distributed solve_vector: this rank passes its rows of the marginals and
-    gets (report, state-of-its-rows); the report is identical on all ranks."""
+    gets (report, state-of-its-rows); the report is identical on all ranks.
+    Either a fresh NCCL unique id (a communicator per call) or a
+    SlabCommunicator reused across calls."""
     cfg = cfg if cfg is not None else SolverConfig()
     eng = make_vector_slab_engine(n, graph, cfg, nranks=nranks, rank=rank, unique_id=unique_id,
-                                  precision=precision, device=device)
+                                  precision=precision, device=device, comm=comm)
     try:
         m0, m1 = eng.set_marginals(np.asarray(l0_rows), np.asarray(l1_rows))
         _mass_check(m0, m1)

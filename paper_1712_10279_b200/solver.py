@@ -345,6 +345,10 @@ class CudaEngine:
         buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
         _lib.check(self._lib.otfx_engine_attach_nccl(self._h, buf, nranks, rank))
 
+    def attach_comm(self, comm):
+        """Use a SlabCommunicator (distributed.py) that outlives this engine."""
+        _lib.check(self._lib.otfx_engine_attach_comm(self._h, comm.handle))
+
 
 def nccl_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()

@@ -494,6 +494,13 @@ def test_nccl_single_rank_path():
     np.testing.assert_array_equal(g.hist_array(rep1), g.hist_array(rep2))
     np.testing.assert_array_equal(st1.phi, st2.phi)
     np.testing.assert_array_equal(st1.w.values, st2.w.values)
+    # a communicator that outlives the engines of several solves
+    comm = D.SlabCommunicator(pk.solver.nccl_unique_id(), 1, 0, 0)
+    for _ in range(2):
+        rep3, st3 = D.solve_vector_rows(l0, l1, gph, n, cfg, nranks=1, rank=0, comm=comm)
+        np.testing.assert_array_equal(g.hist_array(rep3), g.hist_array(rep2))
+        np.testing.assert_array_equal(st3.phi, st2.phi)
+    comm.close()
 
 
 @pytest.mark.parametrize("warps", ["4", "8"])
