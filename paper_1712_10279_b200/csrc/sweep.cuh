@@ -76,8 +76,12 @@ __device__ __forceinline__ int64_t cell_off(const SweepArgs<T>& A, int g, int co
   return int64_t(g - A.row_begin + 1) * A.pitch + col;
 }
 
+// Scalar / vector payloads with k <= 3 are held to 4 resident CTAs per SM
+// (<= 128 registers): small grids run one row per CTA and need every CTA of a
+// 256^2 grid (512) resident in one wave.
 template <class P, typename T, bool CHECK>
-__global__ void __launch_bounds__(128) sweep_kernel(const __grid_constant__ SweepArgs<T> A) {
+__global__ void __launch_bounds__(128, ((P::NCOEF > 0 || !P::HAS_W) && P::K <= 3) ? 4 : 0)
+    sweep_kernel(const __grid_constant__ SweepArgs<T> A) {
   constexpr int NP = P::NP;
   constexpr int NWA = P::NWA;
   constexpr int NARR = CHECK ? 3 : 2;
@@ -113,46 +117,91 @@ __global__ void __launch_bounds__(128) sweep_kernel(const __grid_constant__ Swee
 
   double acc[4] = {0.0, 0.0, 0.0, 0.0};  // SDU, SDW, SDPHI, SCROSS
 
+  // inputs of one row step: phi(i+1), u(i), diff(i), w(i) of this column, and
+  // for the edge threads the halo columns (thread 0: phi(i+1, c0-1),
+  // u(i, c0-1); thread TX-1: phi(i+1, c0+TX))
+  struct RowIn {
+    T phn[NP], uo[2][NP], df[NP], wo[NWA], hphn[NP], huo[2][NP], phr[NP];
+  };
+  auto load_row = [&](int i, RowIn& r) {
+    const bool hasx = i + 1 < n;
+    const int64_t o = cell_off(A, i, j);
+    const int64_t on = cell_off(A, i + 1, j);
+#pragma unroll
+    for (int c = 0; c < NP; ++c) {
+      r.phn[c] = (live && hasx) ? ldg(A.a.phi + c * pl + on) : T(0);
+      r.uo[0][c] = live ? ldg(A.a.u + c * pl + o) : T(0);
+      r.uo[1][c] = live ? ldg(A.a.u + (NP + c) * pl + o) : T(0);
+      r.df[c] = live ? ldg(A.diff + c * pl + o) : T(0);
+    }
+    if (P::HAS_W) {
+#pragma unroll
+      for (int e = 0; e < NWA; ++e)
+        r.wo[e] = (live && e < A.ell * P::NWS) ? ldg(A.a.w + e * pl + o) : T(0);
+    }
+    if (halo_l) {
+      const int64_t oh = cell_off(A, i, c0 - 1), ohn = cell_off(A, i + 1, c0 - 1);
+#pragma unroll
+      for (int c = 0; c < NP; ++c) {
+        r.hphn[c] = hasx ? ldg(A.a.phi + c * pl + ohn) : T(0);
+        r.huo[0][c] = ldg(A.a.u + c * pl + oh);
+        r.huo[1][c] = ldg(A.a.u + (NP + c) * pl + oh);
+      }
+    }
+    if (halo_r) {
+#pragma unroll
+      for (int c = 0; c < NP; ++c)
+        r.phr[c] = hasx ? ldg(A.a.phi + c * pl + cell_off(A, i + 1, c0 + TX)) : T(0);
+    }
+  };
+
   // ---------------------------------------------------------------- prologue
+  // Every global load of the tile's first step is issued up front (first
+  // row's inputs, phi of rows gr0 and gr0-1, u of row gr0-1): small grids run
+  // one row per CTA, where a chain of dependent load rounds is the latency.
+  RowIn in;
+  load_row(gr0, in);
   {
     const int64_t o = cell_off(A, gr0, j);
+    const int gm = gr0 - 1;
+    const int64_t om = cell_off(A, gm, j);
+    T pm[NP], uom[2][NP], pmr[NP], phr0[NP];
 #pragma unroll
     for (int c = 0; c < NP; ++c) {
       phc[c] = live ? ldg(A.a.phi + c * pl + o) : T(0);
-      S(sphi, gr0 & 1, c, t) = phc[c];
-      if (halo_r) S(sphi, gr0 & 1, c, TX) = ldg(A.a.phi + c * pl + cell_off(A, gr0, c0 + TX));
+      if (halo_r) phr0[c] = ldg(A.a.phi + c * pl + cell_off(A, gr0, c0 + TX));
       if (halo_l) hph[c] = ldg(A.a.phi + c * pl + cell_off(A, gr0, c0 - 1));
+      if (gr0 > 0) {
+        pm[c] = live ? ldg(A.a.phi + c * pl + om) : T(0);
+        if (halo_r) pmr[c] = ldg(A.a.phi + c * pl + cell_off(A, gm, c0 + TX));
+        uom[0][c] = live ? ldg(A.a.u + c * pl + om) : T(0);
+        uom[1][c] = live ? ldg(A.a.u + (NP + c) * pl + om) : T(0);
+      }
     }
 #pragma unroll
     for (int c = 0; c < NP; ++c) {
+      S(sphi, gr0 & 1, c, t) = phc[c];
+      if (halo_r) S(sphi, gr0 & 1, c, TX) = phr0[c];
       uxb_prev[c] = T(0);
       dux_prev[c] = T(0);
     }
     if (gr0 > 0) {
       // halo row gr0-1: recompute u'(gr0-1, j) from the read-only iterate
-      const int gm = gr0 - 1;
-      const int64_t om = cell_off(A, gm, j);
-      T pm[NP];
 #pragma unroll
       for (int c = 0; c < NP; ++c) {
-        pm[c] = live ? ldg(A.a.phi + c * pl + om) : T(0);
         S(sphi, gm & 1, c, t) = pm[c];
-        if (halo_r) S(sphi, gm & 1, c, TX) = ldg(A.a.phi + c * pl + cell_off(A, gm, c0 + TX));
+        if (halo_r) S(sphi, gm & 1, c, TX) = pmr[c];
       }
       __syncthreads();
       if (live) {
-        T uo[2][NP], un[2][NP], py[NP];
+        T un[2][NP], py[NP];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) py[c] = hasy ? S(sphi, gm & 1, c, t + 1) : T(0);
+        Cell<P, T>::flux(pm, phc, py, true, hasy, uom, un, A);
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
-          uo[0][c] = ldg(A.a.u + c * pl + om);
-          uo[1][c] = ldg(A.a.u + (NP + c) * pl + om);
-          py[c] = hasy ? S(sphi, gm & 1, c, t + 1) : T(0);
-        }
-        Cell<P, T>::flux(pm, phc, py, true, hasy, uo, un, A);
-#pragma unroll
-        for (int c = 0; c < NP; ++c) {
-          uxb_prev[c] = (un[0][c] + un[0][c]) - uo[0][c];
-          dux_prev[c] = un[0][c] - uo[0][c];
+          uxb_prev[c] = (un[0][c] + un[0][c]) - uom[0][c];
+          dux_prev[c] = un[0][c] - uom[0][c];
         }
       }
     }
@@ -164,35 +213,17 @@ __global__ void __launch_bounds__(128) sweep_kernel(const __grid_constant__ Swee
     const int b = i & 1, bn = (i + 1) & 1;
     const bool hasx = i + 1 < n;
     const int64_t o = cell_off(A, i, j);
-    const int64_t on = cell_off(A, i + 1, j);
-    T phn[NP], uo[2][NP], wo[NWA], df[NP];
-#pragma unroll
-    for (int c = 0; c < NP; ++c) {
-      phn[c] = (live && hasx) ? ldg(A.a.phi + c * pl + on) : T(0);
-      uo[0][c] = live ? ldg(A.a.u + c * pl + o) : T(0);
-      uo[1][c] = live ? ldg(A.a.u + (NP + c) * pl + o) : T(0);
-      df[c] = live ? ldg(A.diff + c * pl + o) : T(0);
-    }
-    if (P::HAS_W) {
-#pragma unroll
-      for (int e = 0; e < NWA; ++e)
-        wo[e] = (live && e < A.ell * P::NWS) ? ldg(A.a.w + e * pl + o) : T(0);
-    }
-    // left halo column inputs (thread 0 only)
-    T hphn[NP], huo[2][NP];
-    if (halo_l) {
-      const int64_t oh = cell_off(A, i, c0 - 1), ohn = cell_off(A, i + 1, c0 - 1);
-#pragma unroll
-      for (int c = 0; c < NP; ++c) {
-        hphn[c] = hasx ? ldg(A.a.phi + c * pl + ohn) : T(0);
-        huo[0][c] = ldg(A.a.u + c * pl + oh);
-        huo[1][c] = ldg(A.a.u + (NP + c) * pl + oh);
-      }
-    }
+    if (i > gr0) load_row(i, in);
+    const T (&phn)[NP] = in.phn;
+    const T (&uo)[2][NP] = in.uo;
+    const T (&df)[NP] = in.df;
+    const T (&wo)[NWA] = in.wo;
+    const T (&hphn)[NP] = in.hphn;
+    const T (&huo)[2][NP] = in.huo;
 #pragma unroll
     for (int c = 0; c < NP; ++c) {
       S(sphi, bn, c, t) = phn[c];
-      if (halo_r) S(sphi, bn, c, TX) = hasx ? ldg(A.a.phi + c * pl + cell_off(A, i + 1, c0 + TX)) : T(0);
+      if (halo_r) S(sphi, bn, c, TX) = in.phr[c];
     }
 
     // spatial flux of this cell
