@@ -653,3 +653,32 @@ def test_local_slab_run_loop_matches_single_engine(monkeypatch, P, n, force_tma,
         assert np.array_equal(cat, ref_arr), q
     for e in reversed(slabs):
         e.close()
+
+
+# ---------------------------------------------------------------------------
+# the bench workload itself (BASELINE configs[4], vector 3-channel 8192^2):
+# the TMA-streamed headline kernel (fused check + speculative dual sweep) and
+# the register-streamed sweep (pinned bit-exact to the reference goldens at
+# small sizes) give the same bits at full size; ghost entries stay zero
+# ---------------------------------------------------------------------------
+def test_bench_size_tma_matches_register_sweep(monkeypatch):
+    n = 8192
+    l0, l1 = synthetic.rgb_disk_pair(n)
+    cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", alpha=0.3, tol_gap=1e-300,
+                          tol_feas=1e-300, max_iters=5, check_every=2)
+    outs = []
+    for tma in ("1", "0"):
+        monkeypatch.setenv("OTFX_TMA", tma)
+        eng = build_engine("vector", n, cfg, graph=pk.triangle_graph())
+        assert (eng.info()["tma_stages"] > 0) == (tma == "1")
+        eng.set_marginals(l0, l1)
+        hist, it, conv, _ = eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+        ux, uy, w, phi = eng.get_state()
+        eng.close()
+        assert it == 5 and not conv
+        assert not ux[n - 1].any() and not uy[:, n - 1].any()  # ghost entries (S/spatial.py:80-86)
+        outs.append((g.hist_array(pk.SolveReport(conv, it, 0.0, hist)), phi, w, ux))
+        del uy
+    (h1, p1, w1, x1), (h2, p2, w2, x2) = outs
+    g.hist_close(h1, h2, 1e-12)
+    assert np.array_equal(p1, p2) and np.array_equal(w1, w2) and np.array_equal(x1, x2)
