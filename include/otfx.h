@@ -115,6 +115,7 @@ typedef struct {
   int32_t regs_tb2;      /* registers per thread of the two-level sweep */
   int32_t smem_tb2;      /* dynamic shared memory per two-level CTA */
   int32_t cluster_ctas;  /* > 0: run()/step() execute on chip in one cluster of this many CTAs */
+  int32_t halo_overlap;  /* slab halo exchange overlapped with the interior bands when decomposed */
 } otfx_engine_info;
 
 int otfx_abi_version(void);

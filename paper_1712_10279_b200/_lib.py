@@ -50,7 +50,7 @@ class EngineInfo(C.Structure):
                 ("grid_y", C.c_int32), ("regs_plain", C.c_int32), ("regs_check", C.c_int32),
                 ("graphs", C.c_int32), ("tma_stages", C.c_int32), ("smem_bytes", C.c_int32),
                 ("tb2", C.c_int32), ("regs_tb2", C.c_int32), ("smem_tb2", C.c_int32),
-                ("cluster_ctas", C.c_int32)]
+                ("cluster_ctas", C.c_int32), ("halo_overlap", C.c_int32)]
 
 
 _P = C.c_void_p

@@ -61,6 +61,8 @@ struct SweepArgs {
   int row_begin;         // first owned global row
   int row_end;           // one past the last owned global row
   int rows_per_block;    // sweep length of one CTA
+  int band0, band_step;  // CTA row y covers band band0 + y * band_step (a launch
+                         // may cover a subset of the slab's bands)
   int ell;               // active channel count (edges / Lindblad matrices)
   int norm_u, norm_w;
   T mu, thr_w, tau, nu, inv_dx;

@@ -311,6 +311,9 @@ struct otfx_engine {
   bool own_comm = false;  // created by attach_nccl (destroyed with the engine)
   int nranks = 1, rank = 0;
   void* d_halo = nullptr;  // send/recv buffers
+  // overlapped halo exchange: edge bands + exchange on a high-priority stream
+  cudaStream_t edge_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // TMA-streamed sweep
   bool use_tma = false;
   otfx::StageLayout L{};
@@ -348,6 +351,8 @@ static SweepArgs<T> make_args(otfx_engine* e, int from) {
   a.row_begin = e->d.row_begin;
   a.row_end = e->d.row_end;
   a.rows_per_block = e->R;
+  a.band0 = 0;
+  a.band_step = 1;
   a.ell = e->d.ell;
   a.norm_u = e->d.norm_u;
   a.norm_w = e->d.norm_w;
@@ -385,22 +390,38 @@ const Ops<double>* ops_of<double>(otfx_engine* e) { return e->ops64; }
 template <>
 const Ops<float>* ops_of<float>(otfx_engine* e) { return e->ops32; }
 
-// fl bit 0: check sweep; bit 1: dual-norm accumulation (TMA sweep only)
+// fl bit 0: check sweep; bit 1: dual-norm accumulation (TMA sweep only).
+// One launch over nb bands (band0, band0 + step, ...) of the slab on stream s;
+// the iterate index is not advanced.
 template <typename T>
-static void launch_sweep(otfx_engine* e, int fl) {
+static void launch_bands(otfx_engine* e, int fl, int band0, int step, int nb, cudaStream_t s) {
   if (e->use_tma) {
     TmaSweepArgs<T> g;
     g.s = make_args<T>(e, e->cur);
+    g.s.band0 = band0;
+    g.s.band_step = step;
     g.L = e->L;
-    CK(ops_of<T>(e)->sweep_tma(g, e->maps[e->cur], dim3(e->gx, e->gy), dim3(32 * (e->L.cw + 1)),
-                               e->stream, fl));
+    CK(ops_of<T>(e)->sweep_tma(g, e->maps[e->cur], dim3(e->gx, nb), dim3(32 * (e->L.cw + 1)), s,
+                               fl));
   } else {
     require((fl & 2) == 0, OTFX_EINVAL, "dual accumulation needs the TMA sweep");
     const bool check = (fl & 1) != 0;
     SweepArgs<T> a = make_args<T>(e, e->cur);
-    CK(ops_of<T>(e)->sweep(a, dim3(e->gx, e->gy), dim3(e->TX),
-                           check ? e->smem_check : e->smem_plain, e->stream, check));
+    a.band0 = band0;
+    a.band_step = step;
+    CK(ops_of<T>(e)->sweep(a, dim3(e->gx, nb), dim3(e->TX),
+                           check ? e->smem_check : e->smem_plain, s, check));
   }
+}
+
+static void launch_bands(otfx_engine* e, int fl, int band0, int step, int nb, cudaStream_t s) {
+  if (e->elem == 8) launch_bands<double>(e, fl, band0, step, nb, s);
+  else launch_bands<float>(e, fl, band0, step, nb, s);
+}
+
+template <typename T>
+static void launch_sweep(otfx_engine* e, int fl) {
+  launch_bands<T>(e, fl, 0, 1, e->gy, e->stream);
   e->cur ^= 1;
 }
 
@@ -538,7 +559,7 @@ static void copy_rows(otfx_engine* dst, void* dbase, int drow, otfx_engine* src,
                        nplanes, cudaMemcpyDeviceToDevice, s));
 }
 
-static void exchange_nccl(otfx_engine* e) {
+static void exchange_nccl(otfx_engine* e, cudaStream_t st) {
   if (!e->comm || e->nranks == 1) return;
   NcclApi& N = nccl();
   const int c = e->cur;
@@ -555,43 +576,91 @@ static void exchange_nccl(otfx_engine* e) {
     return static_cast<char*>(base) + size_t(lrow) * e->pitch * e->elem;
   };
   const bool has_prev = e->rank > 0, has_next = e->rank + 1 < e->nranks;
-  if (has_prev) CK(cudaMemcpy2DAsync(send_top, wb, rowp(e->phi[c], 1), pb, wb, NP, cudaMemcpyDeviceToDevice, e->stream));
+  if (has_prev) CK(cudaMemcpy2DAsync(send_top, wb, rowp(e->phi[c], 1), pb, wb, NP, cudaMemcpyDeviceToDevice, st));
   if (has_next) {
-    CK(cudaMemcpy2DAsync(send_bot, wb, rowp(e->phi[c], e->rows), pb, wb, NP, cudaMemcpyDeviceToDevice, e->stream));
+    CK(cudaMemcpy2DAsync(send_bot, wb, rowp(e->phi[c], e->rows), pb, wb, NP, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpy2DAsync(send_bot + NP * wb, wb, rowp(e->u[c], e->rows), pb, wb, 2 * NP,
-                         cudaMemcpyDeviceToDevice, e->stream));
+                         cudaMemcpyDeviceToDevice, st));
   }
   const ncclDataType_t dt = e->elem == 8 ? ncclFloat64 : ncclFloat32;
   NK(N.GroupStart());
   if (has_prev) {
-    NK(N.Send(send_top, NP * w, dt, e->rank - 1, e->comm, e->stream));
-    NK(N.Recv(recv_top, 3 * NP * w, dt, e->rank - 1, e->comm, e->stream));
+    NK(N.Send(send_top, NP * w, dt, e->rank - 1, e->comm, st));
+    NK(N.Recv(recv_top, 3 * NP * w, dt, e->rank - 1, e->comm, st));
   }
   if (has_next) {
-    NK(N.Send(send_bot, 3 * NP * w, dt, e->rank + 1, e->comm, e->stream));
-    NK(N.Recv(recv_bot, NP * w, dt, e->rank + 1, e->comm, e->stream));
+    NK(N.Send(send_bot, 3 * NP * w, dt, e->rank + 1, e->comm, st));
+    NK(N.Recv(recv_bot, NP * w, dt, e->rank + 1, e->comm, st));
   }
   NK(N.GroupEnd());
   if (has_prev) {
-    CK(cudaMemcpy2DAsync(rowp(e->phi[c], 0), pb, recv_top, wb, wb, NP, cudaMemcpyDeviceToDevice, e->stream));
+    CK(cudaMemcpy2DAsync(rowp(e->phi[c], 0), pb, recv_top, wb, wb, NP, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpy2DAsync(rowp(e->u[c], 0), pb, recv_top + NP * wb, wb, wb, 2 * NP,
-                         cudaMemcpyDeviceToDevice, e->stream));
+                         cudaMemcpyDeviceToDevice, st));
   }
   if (has_next)
     CK(cudaMemcpy2DAsync(rowp(e->phi[c], e->rows + 1), pb, recv_bot, wb, wb, NP,
-                         cudaMemcpyDeviceToDevice, e->stream));
+                         cudaMemcpyDeviceToDevice, st));
 }
 
+
+static void exchange_nccl(otfx_engine* e) { exchange_nccl(e, e->stream); }
+
+// ---- halo exchange overlapped with the interior -------------------------------
+// Every iteration of a decomposed slab: the two edge bands (first and last
+// row band, which produce the rows the neighbours need and read the ghost
+// rows) run on a high-priority edge stream, followed there by the halo
+// exchange; the interior bands run concurrently on the engine stream.  Both
+// halves read iterate k and write disjoint rows of iterate k+1; the exchange
+// reads the edge bands' boundary rows of k+1 and writes its ghost rows, which
+// no interior band touches.  The engine stream then joins the edge stream, so
+// the exchange of iteration k is hidden behind the interior of iteration k.
+static bool overlap_ready(const otfx_engine* e) {
+  return e->gy >= 3 && !e->use_tb2 && env_int("OTFX_OVERLAP", 1) != 0;
+}
+
+static void ensure_overlap(otfx_engine* e) {
+  if (e->edge_stream) return;
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CK(cudaStreamCreateWithPriority(&e->edge_stream, cudaStreamNonBlocking, hi));
+  CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
+}
+
+// one overlapped iteration of the engines es[0..count) (one rank's slab, or a
+// local group sharing es[0]'s stream); `exchange` runs on the edge stream
+template <class X>
+static void overlapped_sweep(otfx_engine* const* es, int count, int fl, X&& exchange) {
+  otfx_engine* L = es[0];
+  ensure_overlap(L);
+  CK(cudaEventRecord(L->ev_fork, L->stream));
+  CK(cudaStreamWaitEvent(L->edge_stream, L->ev_fork, 0));
+  for (int q = 0; q < count; ++q) launch_bands(es[q], fl, 0, es[q]->gy - 1, 2, L->edge_stream);
+  for (int q = 0; q < count; ++q) launch_bands(es[q], fl, 1, 1, es[q]->gy - 2, L->stream);
+  for (int q = 0; q < count; ++q) es[q]->cur ^= 1;
+  exchange(L->edge_stream);
+  CK(cudaEventRecord(L->ev_join, L->edge_stream));
+  CK(cudaStreamWaitEvent(L->stream, L->ev_join, 0));
+}
+
+// one iteration of a rank's slab followed by its halo exchange
+static void sweep_exchange(otfx_engine* e, int fl) {
+  if (e->comm && e->nranks > 1 && overlap_ready(e)) {
+    otfx_engine* const one[1] = {e};
+    overlapped_sweep(one, 1, fl, [&](cudaStream_t st) { exchange_nccl(e, st); });
+    return;
+  }
+  launch_sweep(e, fl);
+  exchange_nccl(e);
+}
 
 static void enqueue_plain(otfx_engine* e, int64_t count) {
   int64_t q = 0;
   if (e->use_tb2) {
     for (; q + 2 <= count; q += 2) launch_tb2(e);
   }
-  for (; q < count; ++q) {
-    launch_sweep(e, 0);
-    exchange_nccl(e);
-  }
+  for (; q < count; ++q) sweep_exchange(e, 0);
 }
 
 // buffer flips of enqueue_plain(count)
@@ -1388,6 +1457,12 @@ static void destroy(otfx_engine* e) {
     cudaEventDestroy(pr.second);
   }
   if (e->stream) cudaStreamSynchronize(e->stream);
+  if (e->edge_stream) {
+    cudaStreamSynchronize(e->edge_stream);
+    cudaStreamDestroy(e->edge_stream);
+  }
+  if (e->ev_fork) cudaEventDestroy(e->ev_fork);
+  if (e->ev_join) cudaEventDestroy(e->ev_join);
   if (e->comm && e->own_comm && nccl().CommDestroy) nccl().CommDestroy(e->comm);
   if (e->mem) {
     if (e->pooled) {
@@ -1431,7 +1506,7 @@ struct SlabGroup {
   otfx_engine* lead() const { return es[0]; }
 };
 
-static void exchange_local_impl(otfx_engine* const* es, int count) {
+static void exchange_local_impl(otfx_engine* const* es, int count, cudaStream_t st) {
   for (int s = 0; s + 1 < count; ++s) {
     otfx_engine* a = es[s];
     otfx_engine* b = es[s + 1];
@@ -1442,18 +1517,29 @@ static void exchange_local_impl(otfx_engine* const* es, int count) {
     require(a->cur == b->cur, OTFX_EINVAL, "engines are at different iterations");
     const int c = a->cur;
     // a's bottom ghost <- b's first row (phi)
-    copy_rows(a, a->phi[c], a->rows + 1, b, b->phi[c], 1, a->NP, a->stream);
+    copy_rows(a, a->phi[c], a->rows + 1, b, b->phi[c], 1, a->NP, st);
     // b's top ghost <- a's last row (phi, u)
-    copy_rows(b, b->phi[c], 0, a, a->phi[c], a->rows, a->NP, a->stream);
-    copy_rows(b, b->u[c], 0, a, a->u[c], a->rows, 2 * a->NP, a->stream);
+    copy_rows(b, b->phi[c], 0, a, a->phi[c], a->rows, a->NP, st);
+    copy_rows(b, b->u[c], 0, a, a->u[c], a->rows, 2 * a->NP, st);
   }
 }
 
-// one iteration of every slab, then the halo exchange
+// one iteration of every slab, then the halo exchange (overlapped with the
+// interior bands when the slabs are tall enough)
 static void group_sweep(const SlabGroup& g, int fl) {
+  if (!g.local()) {
+    sweep_exchange(g.lead(), fl);
+    return;
+  }
+  bool ov = true;
+  for (int q = 0; q < g.count; ++q) ov = ov && overlap_ready(g.es[q]);
+  if (ov) {
+    overlapped_sweep(g.es, g.count, fl,
+                     [&](cudaStream_t st) { exchange_local_impl(g.es, g.count, st); });
+    return;
+  }
   for (int q = 0; q < g.count; ++q) launch_sweep(g.es[q], fl);
-  if (g.local()) exchange_local_impl(g.es, g.count);
-  else exchange_nccl(g.lead());
+  exchange_local_impl(g.es, g.count, g.lead()->stream);
 }
 
 static void group_plain(const SlabGroup& g, int64_t count) {
@@ -1615,6 +1701,7 @@ int otfx_engine_get_info(otfx_engine* e, otfx_engine_info* info) {
   info->smem_tb2 = e->use_tb2 ? e->L2.total : 0;
   info->smem_bytes = e->use_tma ? e->L.total : int(e->smem_plain);
   info->cluster_ctas = cluster_ok(e) ? e->cl_ctas : 0;
+  info->halo_overlap = overlap_ready(e) ? 1 : 0;
   if (e->use_tma) {
     info->regs_plain = e->ops64 ? e->ops64->tma_regs(false) : e->ops32->tma_regs(false);
     info->regs_check = e->ops64 ? e->ops64->tma_regs(true) : e->ops32->tma_regs(true);
@@ -1738,8 +1825,7 @@ int otfx_engine_step_check(otfx_engine* e, double out[5]) {
   API_BEGIN
   require(e && out, OTFX_EINVAL, "null pointer");
   CK(cudaSetDevice(e->d.device));
-  launch_sweep(e, 1);
-  exchange_nccl(e);
+  sweep_exchange(e, 1);
   raw_to_host(e, true, true);
   finalize(e, e->h_raw, out);
   API_END
@@ -1867,7 +1953,7 @@ int otfx_engine_exchange_local(otfx_engine* const* es, int count) {
   API_BEGIN
   require(es && count >= 1, OTFX_EINVAL, "no engines");
   CK(cudaSetDevice(es[0]->d.device));
-  exchange_local_impl(es, count);
+  exchange_local_impl(es, count, es[0]->stream);
   API_END
 }
 

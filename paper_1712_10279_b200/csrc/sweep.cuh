@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(128, ((P::NCOEF > 0 || !P::HAS_W) && P::K <= 3
   const int n = A.n;
   const bool live = j < n;
   const bool hasy = j + 1 < n;
-  const int gr0 = A.row_begin + blockIdx.y * A.rows_per_block;
+  const int band = A.band0 + int(blockIdx.y) * A.band_step;
+  const int gr0 = A.row_begin + band * A.rows_per_block;
   const int gr1 = min(gr0 + A.rows_per_block, A.row_end);
   const int64_t pl = A.plane;
   const bool halo_l = (t == 0) && (c0 > 0);
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(128, ((P::NCOEF > 0 || !P::HAS_W) && P::K <= 3
   if (CHECK) {
     block_sum<4>(acc, sred);
     if (t == 0) {
-      double* dst = A.partials + (size_t(blockIdx.y) * gridDim.x + blockIdx.x) * 10;
+      double* dst = A.partials + (size_t(band) * gridDim.x + blockIdx.x) * 10;
 #pragma unroll
       for (int s = 0; s < 4; ++s) dst[s] = acc[s];
 #pragma unroll

@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
   const int n = A.n;
   const bool out = !producer && lane > 0 && j < n;  // lane 0 is the overlap column
   const bool hasy = j + 1 < n;
-  const int gr0 = A.row_begin + blockIdx.y * A.rows_per_block;
+  const int band = A.band0 + int(blockIdx.y) * A.band_step;
+  const int gr0 = A.row_begin + band * A.rows_per_block;
   const int gr1 = min(gr0 + A.rows_per_block, A.row_end);
   const int qbase = gr0 - 1;
   const int qmax = gr1 - qbase;  // index of the phi-only tail stage
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
     }
   }
 
-  const size_t bid = size_t(blockIdx.y) * gridDim.x + blockIdx.x;
+  const size_t bid = size_t(band) * gridDim.x + blockIdx.x;
   if (CHECK) {
     block_sum<10>(acc, sred);
     if (t == 0) {

@@ -612,11 +612,16 @@ def test_pooled_engines_reuse_memory_and_release():
 # rule) over P row slabs of one grid on one GPU, with the TMA-streamed slab
 # sweeps the multi-GPU bench runs: same iterates and history as one engine
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("overlap", ["1", "0"])
 @pytest.mark.parametrize("P,n,force_tma,conv", [
     (2, 300, True, False), (3, 301, True, False), (2, 1100, False, False), (2, 32, True, True),
+    (4, 900, True, False),
 ])
-def test_local_slab_run_loop_matches_single_engine(monkeypatch, P, n, force_tma, conv):
+def test_local_slab_run_loop_matches_single_engine(monkeypatch, P, n, force_tma, conv, overlap):
+    """overlap=1: edge bands + halo exchange on the high-priority stream,
+    interior bands concurrently on the engine stream (the multi-GPU schedule)."""
     from paper_1712_10279_b200.solver import run_local
+    monkeypatch.setenv("OTFX_OVERLAP", overlap)
     if force_tma:
         monkeypatch.setenv("OTFX_TMA", "1")
     l0, l1 = synthetic.rgb_disk_pair(n)
@@ -637,6 +642,7 @@ def test_local_slab_run_loop_matches_single_engine(monkeypatch, P, n, force_tma,
     for r in range(P):
         e = build_engine("vector", n, cfg, graph=gph, rows=(bounds[r], bounds[r + 1]), stream=stream)
         assert e.info()["tma_stages"] > 0
+        assert e.info()["halo_overlap"] == (1 if overlap == "1" and e.info()["grid_y"] >= 3 else 0)
         stream = e.stream
         e.set_marginals(l0[bounds[r]:bounds[r + 1]], l1[bounds[r]:bounds[r + 1]])
         slabs.append(e)
