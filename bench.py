@@ -258,6 +258,8 @@ def run_ours(args):
     # with temporal blocking one launch (one HBM pass) advances two iterations
     ipl = 2 if info["tb2"] else 1
     sweep_ms = plain_ms / max(plain_iters / ipl, 1)
+    if not sweep_ms > 0:  # no plain iterations timed: fall back to the whole step
+        sweep_ms = ms / max(args.steps * ips / ipl, 1)
     t = torch.tensor([ms, sweep_ms], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -527,6 +529,7 @@ def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn):
     t = torch.tensor([max(times) if False else float(np.mean(times))], device="cuda")
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        comm.close()  # every rank, same point
     sec = float(t[0])
     cells = float(n) * n
     rows_cells = float(r1 - r0) * n

@@ -668,12 +668,37 @@ static int64_t plain_flips(const otfx_engine* e, int64_t count) {
   return e->use_tb2 ? count / 2 + count % 2 : count;
 }
 
+// device-time bracket (CUDA events on the engine stream) around a run of
+// plain iterations, folded into plain_ms by collect_timing
+static int timing_begin(otfx_engine* e) {
+  if (!e->timing) return -1;
+  const int slot = int(e->ev_pending.size());
+  while (int(e->ev_pool.size()) <= slot) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    e->ev_pool.emplace_back(a, b);
+  }
+  CK(cudaEventRecord(e->ev_pool[slot].first, e->stream));
+  return slot;
+}
+
+static void timing_end(otfx_engine* e, int slot, int64_t count) {
+  if (slot < 0) return;
+  CK(cudaEventRecord(e->ev_pool[slot].second, e->stream));
+  e->ev_pending.emplace_back(slot, count);
+}
+
 static void run_plain(otfx_engine* e, int64_t count) {
   if (count <= 0) return;
   // NCCL halo exchanges stay outside graph capture unless explicitly enabled
   const bool graphs = e->use_graphs && (e->nranks == 1 || env_int("OTFX_NCCL_GRAPHS", 0) != 0);
   if (!graphs || count < 3) {
+    // (timed too: a decomposed slab runs here, its iterations including the
+    // overlapped halo exchange)
+    const int slot = timing_begin(e);
     enqueue_plain(e, count);
+    timing_end(e, slot, count);
     return;
   }
   auto key = std::make_pair(e->cur, count);

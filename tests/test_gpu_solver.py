@@ -688,3 +688,19 @@ def test_bench_size_tma_matches_register_sweep(monkeypatch):
     (h1, p1, w1, x1), (h2, p2, w2, x2) = outs
     g.hist_close(h1, h2, 1e-12)
     assert np.array_equal(p1, p2) and np.array_equal(w1, w2) and np.array_equal(x1, x2)
+
+
+def test_engine_timing_covers_ungraphed_runs(monkeypatch):
+    """The bench's sweep timing also brackets plain iterations launched
+    without a CUDA graph (the path a decomposed slab takes)."""
+    monkeypatch.setenv("OTFX_GRAPHS", "0")
+    l0, l1 = synthetic.rgb_disk_pair(600)
+    cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", tol_gap=1e-300, tol_feas=1e-300,
+                          max_iters=200, check_every=100)
+    eng = build_engine("vector", 600, cfg, graph=pk.triangle_graph())
+    eng.set_marginals(l0, l1)
+    eng.timing(1)
+    eng.run(1e-300, 1e-300, 200, 100)
+    ms, iters = eng.timing(0)
+    eng.close()
+    assert iters >= 190 and ms > 0
