@@ -156,3 +156,26 @@ def test_slab_bounds_cover_grid(n, P):
             assert p["bottom"]["row"] == b[r + 1] == plan[r + 1]["rows"][0]
     with pytest.raises(ValueError):
         slab_bounds(3, 4)
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the CPU reference arm the driver runs): one
+    JSON line with the contract keys on rank 0; other ranks exit 0 silently."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
+           "--warmup", "1", "--ref-n", "48"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, check=True)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "cpu_baseline", "e2e", "config"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env,
+                         check=True)
+    assert out.stdout.strip() == ""
