@@ -215,8 +215,9 @@ __global__ void reduce_raw_kernel(const double* __restrict__ pe, const double* _
   }
 }
 
-// Fused check: R^k, primal and feasibility partials of the check sweep
-// ([nb][10]) and the dual-norm partials of the following sweep ([nb][4]).
+// Fused check: R^k partials of the check sweep ([nb][10], slots 0..3) and the
+// evaluate partials of the following sweep ([nb][10]: PU PW SU2 SW2 SCON SPHID
+// PENU PENW | GU GW), reduced in block order.
 __global__ void reduce_fused_kernel(const double* __restrict__ pc, const double* __restrict__ pd,
                                     int nb, double* raw) {
   __shared__ double sred[32 * 12];
@@ -224,21 +225,21 @@ __global__ void reduce_fused_kernel(const double* __restrict__ pc, const double*
   for (int q = 0; q < 12; ++q) v[q] = 0.0;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     const double* c = pc + size_t(b) * 10;
-    const double* d = pd + size_t(b) * 4;
+    const double* d = pd + size_t(b) * 10;
     v[R_SDU] += c[0];
     v[R_SDW] += c[1];
     v[R_SDPHI] += c[2];
     v[R_SCROSS] += c[3];
-    v[R_PU] += c[4];
-    v[R_PW] += c[5];
-    v[R_SU2] += c[6];
-    v[R_SW2] += c[7];
-    v[R_SCON] += c[8];
-    v[R_SPHID] += c[9];
-    v[R_PENU] += d[0];
-    v[R_PENW] += d[1];
-    mx[0] = dmax(mx[0], d[2]);
-    mx[1] = dmax(mx[1], d[3]);
+    v[R_PU] += d[0];
+    v[R_PW] += d[1];
+    v[R_SU2] += d[2];
+    v[R_SW2] += d[3];
+    v[R_SCON] += d[4];
+    v[R_SPHID] += d[5];
+    v[R_PENU] += d[6];
+    v[R_PENW] += d[7];
+    mx[0] = dmax(mx[0], d[8]);
+    mx[1] = dmax(mx[1], d[9]);
   }
   block_sum<12>(v, sred);
   block_max<2>(mx, sred);
@@ -284,7 +285,7 @@ struct otfx_engine {
   size_t smem_plain = 0, smem_check = 0;
   // reductions
   double* d_part_sweep = nullptr;  // [gx*gy][10] check-sweep partials
-  double* d_part_dual = nullptr;   // [gx*gy][4] dual-sweep partials
+  double* d_part_dual = nullptr;   // [gx*gy][10] dual-sweep partials
   double* d_part_eval = nullptr;   // [ex*ey][8]
   double* d_max_eval = nullptr;    // [ex*ey][2]
   double* d_raw = nullptr;         // [OTFX_NRAW]
@@ -1405,7 +1406,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   e->stage_bytes = std::max<size_t>(size_t(128) << 20, size_t(4) * n * max_rec * sizeof(double));
 
   const size_t n_sweep = size_t(e->gx) * e->gy * 10, n_pe = size_t(e->ex) * e->ey * 8,
-               n_me = size_t(e->ex) * e->ey * 2, n_du = size_t(e->gx) * e->gy * 4;
+               n_me = size_t(e->ex) * e->ey * 2, n_du = size_t(e->gx) * e->gy * 10;
   const size_t halo = size_t(8) * NP * n * e->elem;
   size_t off = 0;
   auto carve = [&](size_t bytes) {

@@ -106,11 +106,12 @@ struct StageShape {
 };
 
 // FL bit 0 (CHECK): this sweep ends on a check iteration -- accumulate the
-//   R^k terms plus the primal, feasibility and <phi, diff> terms of the new
-//   iterate (S/solver.py:242-256, 282-291) from registers;
-// FL bit 1 (DUAL): the INPUT iterate is a checked one -- accumulate the dual
-//   norms of its gradients (S/solver.py:258-274), which this sweep computes
-//   anyway for the flux and channel updates.
+//   R^k terms (S/solver.py:282-291) from the old and new values in registers;
+// FL bit 1 (DUAL): the INPUT iterate is a checked one -- accumulate its
+//   evaluate terms (S/solver.py:242-280): primal, feasibility and <phi, diff>
+//   from the staged input, and the dual norms of its gradients, which this
+//   sweep computes anyway for the flux and channel updates.  (Splitting the
+//   check work over the two sweeps keeps both close to a plain sweep.)
 template <class P, typename T, int FL, int CWT = 4>
 //
 // Occupancy hints, measured on B200 (profiles/README.md): the wide check and
@@ -164,9 +165,9 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
   }
   __syncthreads();
 
-  // CHECK: SDU SDW SDPHI SCROSS PU PW SU2 SW2 SCON SPHID;  DUAL: PENU PENW | GU GW
-  double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  double dsum[2] = {0.0, 0.0}, dmx[2] = {0.0, 0.0};
+  // CHECK: SDU SDW SDPHI SCROSS;  DUAL: PU PW SU2 SW2 SCON SPHID PENU PENW | GU GW
+  double acc[4] = {0, 0, 0, 0};
+  double dsum[8] = {0, 0, 0, 0, 0, 0, 0, 0}, dmx[2] = {0.0, 0.0};
   if (producer) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
@@ -227,12 +228,12 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
                      : "memory");
     };
-    T uxb_prev[NP], dux_prev[NP], unx_prev[NP];
+    T uxb_prev[NP], dux_prev[NP], uox_prev[NP];
 #pragma unroll
     for (int c = 0; c < NP; ++c) {
       uxb_prev[c] = T(0);
       dux_prev[c] = T(0);
-      unx_prev[c] = T(0);
+      uox_prev[c] = T(0);
     }
     int s1 = 1, ph1 = 0;  // cursor of stage q+1
     if (S == 1) s1 = 0;
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
       for (int c = 0; c < NP; ++c) {
         uxb_prev[c] = (un[0][c] + un[0][c]) - uo[0][c];
         dux_prev[c] = un[0][c] - uo[0][c];
-        unx_prev[c] = un[0][c];
+        uox_prev[c] = uo[0][c];
       }
     }
     release(s0);
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
       const T* sD = reinterpret_cast<const T*>(st0 + SS::OFF_D);
       const T* sP = reinterpret_cast<const T*>(st0 + SS::OFF_P);
       const T* sPn = reinterpret_cast<const T*>(st1 + SS::OFF_P);
-      T phc[NP], un[2][NP], ub[2][NP], uo[2][NP], lub[NP], ldu[NP], lun[NP];
+      T phc[NP], un[2][NP], ub[2][NP], uo[2][NP], lub[NP], ldu[NP], luo[NP];
       {
         T phx[NP], phy[NP], g[2][NP];
 #pragma unroll
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
           uo[1][c] = sU[(NP + c) * TW];
         }
         Cell<P, T>::grad(phc, phx, phy, hasx, hasy, g, H);
-        if (DUAL && out) P::dual_u(g, H.norm_u, dmx[0], dsum[0]);
+        if (DUAL && out) P::dual_u(g, H.norm_u, dmx[0], dsum[6]);
         Cell<P, T>::flux_g(g, uo, un, H);
 #pragma unroll
         for (int c = 0; c < NP; ++c) {
@@ -300,10 +301,8 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
           ub[1][c] = (un[1][c] + un[1][c]) - uo[1][c];
           // ubar_y / du_y / u'_y of the left neighbour (i, j-1) from lane - 1
           lub[c] = __shfl_up_sync(0xffffffffu, ub[1][c], 1);
-          if (CHECK) {
-            ldu[c] = __shfl_up_sync(0xffffffffu, un[1][c] - uo[1][c], 1);
-            lun[c] = __shfl_up_sync(0xffffffffu, un[1][c], 1);
-          }
+          if (CHECK) ldu[c] = __shfl_up_sync(0xffffffffu, un[1][c] - uo[1][c], 1);
+          if (DUAL) luo[c] = __shfl_up_sync(0xffffffffu, uo[1][c], 1);
         }
       }
       T df[NP], wo[NWA];
@@ -330,7 +329,7 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
         if (P::HAS_W) {
           T gc[NWA];
           P::grad_c(phc, gc, H);
-          if (DUAL) P::dual_w(gc, H.norm_w, H.ell, H.alpha, dmx[1], dsum[1]);
+          if (DUAL) P::dual_w(gc, H.norm_w, H.ell, H.alpha, dmx[1], dsum[7]);
 #pragma unroll
           for (int e = 0; e < NWA; ++e) wn[e] = gc[e] * H.nu + wo[e];
           P::prox_w(wn, H);
@@ -391,48 +390,52 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
             acc[2] += P::wp(c) * double(dp) * double(dp);
             acc[3] += P::wp(c) * double(dp) * double(cross[c]);
           }
-          // primal / feasibility / <phi, diff> of the new iterate
-          acc[4] += P::norm_u(un, H.norm_u);
+        }
+        if (DUAL) {
+          // evaluate terms of the input (checked) iterate, same order as
+          // evaluate_kernel (S/solver.py:242-256)
+          dsum[0] += P::norm_u(uo, H.norm_u);
           T con[NP];
           double su = 0.0, sc2 = 0.0, sp = 0.0;
 #pragma unroll
           for (int c = 0; c < NP; ++c) {
-            su += P::wp(c) * (double(un[0][c]) * double(un[0][c]) +
-                              double(un[1][c]) * double(un[1][c]));
-            T d = un[0][c];
-            if (i > 0) d = d - unx_prev[c];
-            d = d + un[1][c];
-            if (j > 0) d = d - lun[c];
+            su += P::wp(c) * (double(uo[0][c]) * double(uo[0][c]) +
+                              double(uo[1][c]) * double(uo[1][c]));
+            T d = uo[0][c];
+            if (i > 0) d = d - uox_prev[c];
+            d = d + uo[1][c];
+            if (j > 0) d = d - luo[c];
             con[c] = d * H.inv_dx - df[c];
           }
-          acc[6] += su;
+          dsum[2] += su;
           if (P::HAS_W) {
-            acc[5] += P::norm_w(wn, H.norm_w);
+            T wa[NWA];
+#pragma unroll
+            for (int e = 0; e < NWA; ++e) wa[e] = e < nwp ? wo[e] : T(0);
+            dsum[1] += P::norm_w(wa, H.norm_w);
             double sw = 0.0;
 #pragma unroll
-            for (int e = 0; e < NWA; ++e) sw += P::ww(e) * double(wn[e]) * double(wn[e]);
-            acc[7] += sw;
+            for (int e = 0; e < NWA; ++e) sw += P::ww(e) * double(wa[e]) * double(wa[e]);
+            dsum[3] += sw;
             T dv[NP];
-            P::div_c(wn, dv, H);
+            P::div_c(wa, dv, H);
 #pragma unroll
             for (int c = 0; c < NP; ++c) con[c] = con[c] + dv[c];
           }
 #pragma unroll
           for (int c = 0; c < NP; ++c) {
             sc2 += P::wp(c) * double(con[c]) * double(con[c]);
-            sp += P::wp(c) * double(phnew[c]) * double(df[c]);
+            sp += P::wp(c) * double(phc[c]) * double(df[c]);
           }
-          acc[8] += sc2;
-          acc[9] += sp;
+          dsum[4] += sc2;
+          dsum[5] += sp;
         }
       }
 #pragma unroll
       for (int c = 0; c < NP; ++c) {
         uxb_prev[c] = ub[0][c];
-        if (CHECK) {
-          dux_prev[c] = un[0][c] - uo[0][c];
-          unx_prev[c] = un[0][c];
-        }
+        if (CHECK) dux_prev[c] = un[0][c] - uo[0][c];
+        if (DUAL) uox_prev[c] = uo[0][c];
       }
       s0 = s1;
       ph0 = ph1;
@@ -442,22 +445,24 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
 
   const size_t bid = size_t(band) * gridDim.x + blockIdx.x;
   if (CHECK) {
-    block_sum<10>(acc, sred);
+    block_sum<4>(acc, sred);
     if (t == 0) {
       double* dst = A.partials + bid * 10;
 #pragma unroll
-      for (int s = 0; s < 10; ++s) dst[s] = acc[s];
+      for (int s = 0; s < 4; ++s) dst[s] = acc[s];
+#pragma unroll
+      for (int s = 4; s < 10; ++s) dst[s] = 0.0;
     }
   }
   if (DUAL) {
-    block_sum<2>(dsum, sred);
+    block_sum<8>(dsum, sred);
     block_max<2>(dmx, sred);
     if (t == 0) {
-      double* dst = A.dualp + bid * 4;
-      dst[0] = dsum[0];
-      dst[1] = dsum[1];
-      dst[2] = dmx[0];
-      dst[3] = dmx[1];
+      double* dst = A.dualp + bid * 10;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) dst[s] = dsum[s];
+      dst[8] = dmx[0];
+      dst[9] = dmx[1];
     }
   }
 }
