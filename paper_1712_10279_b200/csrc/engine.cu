@@ -14,6 +14,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <omp.h>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -1091,7 +1092,10 @@ static PinnedPool& pinned_pool() {
 }
 
 static void par_copy(void* dst, const void* src, size_t bytes) {
-  const size_t grain = size_t(4) << 20;
+  // ~2 blocks per host thread (first-touch page faults of fresh NumPy
+  // arrays are part of the cost, so every core should take a share)
+  static const int nthr = std::max(1, omp_get_max_threads());
+  const size_t grain = std::max<size_t>(size_t(1) << 20, (bytes / (2 * nthr) + 4095) & ~size_t(4095));
   const long nblk = long((bytes + grain - 1) / grain);
 #pragma omp parallel for schedule(static) if (nblk > 1)
   for (long b = 0; b < nblk; ++b) {
