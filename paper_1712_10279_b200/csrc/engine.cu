@@ -723,22 +723,9 @@ static void run_plain(otfx_engine* e, int64_t count) {
     cudaGraphDestroy(g);
     it = e->graphs.emplace(key, ge).first;
   }
-  int slot = -1;
-  if (e->timing) {
-    slot = int(e->ev_pending.size());
-    while (int(e->ev_pool.size()) <= slot) {
-      cudaEvent_t a, b;
-      CK(cudaEventCreate(&a));
-      CK(cudaEventCreate(&b));
-      e->ev_pool.emplace_back(a, b);
-    }
-    CK(cudaEventRecord(e->ev_pool[slot].first, e->stream));
-  }
+  const int slot = timing_begin(e);
   CK(cudaGraphLaunch(it->second, e->stream));
-  if (e->timing) {
-    CK(cudaEventRecord(e->ev_pool[slot].second, e->stream));
-    e->ev_pending.emplace_back(slot, count);
-  }
+  timing_end(e, slot, count);
   e->cur ^= int(plain_flips(e, count) & 1);
 }
 
