@@ -463,11 +463,15 @@ static int round_up(int x, int a) { return (x + a - 1) / a * a; }
 // shared-memory plan of the TMA sweep; returns false when it cannot fit
 static bool plan_stages(otfx_engine* e, int S) {
   StageLayout& L = e->L;
-  require(S >= 3 && S <= 8, OTFX_EINVAL, "TMA ring depth must be in [3, 8]");
-  // consumer warps per CTA: 8 (248 columns, half the halo re-reads) where the
-  // payload has a wide instantiation, else 4; OTFX_TMA_WARPS overrides
+  // consumer warps per CTA: the payload's wide instantiation (8 warps, 248
+  // columns, half the halo re-reads, for graph payloads; 6 for the heavy
+  // complex matrices), else 4; OTFX_TMA_WARPS=4 overrides
   const int wide = e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw;
-  L.cw = env_int("OTFX_TMA_WARPS", wide) == 8 && wide == 8 ? 8 : 4;
+  L.cw = env_int("OTFX_TMA_WARPS", wide) == wide ? wide : 4;
+  // the consumers hold stages q and q+1, so 2 is the minimum ring; only the
+  // 6-warp heavy payloads use it (their stage is released before the W half
+  // of the row, whose eigensolves cover the next load)
+  require(S >= (L.cw == 6 ? 2 : 3) && S <= 8, OTFX_EINVAL, "TMA ring depth out of range");
   L.tile = 31 * L.cw;  // a multiple of 16 bytes' worth of columns for fp32 and fp64
   L.h = 16 / e->elem;
   L.tw = L.tile + 2 * L.h;
@@ -1310,11 +1314,14 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     // (measured on B200: 2x2 complex l1nuc 75 % -> 88 % of the HBM roofline at
     // 3 stages / 3 CTAs vs 4 stages / 2 CTAs; fp32 vector, 3 CTAs either way:
     // 96 % at 4 stages vs 92 % at 3)
+    // (2 stages are a candidate only for the 6-warp heavy payloads)
+    const int wide = e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw;
+    const int smin = (wide == 6 && env_int("OTFX_TMA_WARPS", wide) == wide) ? 2 : 3;
     int S = env_int("OTFX_STAGES", 0);
     if (S <= 0) {
       CK(e->ops64 ? e->ops64->prepare() : e->ops32->prepare());
       int best = -1;
-      for (int cand = 4; cand >= 3; --cand) {
+      for (int cand = 4; cand >= smin; --cand) {
         if (!plan_stages(e, cand)) continue;
         const int occ = e->ops64 ? e->ops64->tma_occupancy(e->L.cw, e->L.total)
                                  : e->ops32->tma_occupancy(e->L.cw, e->L.total);
@@ -1323,9 +1330,9 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
           S = cand;
         }
       }
-      if (S <= 0) S = 3;
+      if (S <= 0) S = smin;
     }
-    e->use_tma = plan_stages(e, std::max(3, S));
+    e->use_tma = plan_stages(e, std::max(smin, S));
   }
   // two-level sweep (temporal blocking), opt-in with OTFX_TB2=1: on B200 in fp64
   // it is bound by the dependent DP chains (2x the instructions per pass at

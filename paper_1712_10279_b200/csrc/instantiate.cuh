@@ -50,9 +50,13 @@ struct OpsFor {
     }
     return 0;
   }
-  // wide CTAs (8 consumer warps, 248 columns) for the graph payloads; the
-  // matrix payloads keep 4 (their stages are large)
-  static constexpr int WIDE = (P::NCOEF > 0 || !P::HAS_W) ? 8 : 4;
+  // wide CTAs (8 consumer warps, 248 columns) for the graph payloads.  The
+  // fp64 complex-Hermitian payloads with K >= 3 run at ptxas' 255-register cap,
+  // where registers allow 8 warps per SM but a 4-consumer CTA (+ producer)
+  // only 5 resident: they get 6 consumer warps (186 columns, a multiple of 16
+  // bytes of fp64) on a 2-stage ring.  The other matrix payloads keep 4.
+  static constexpr bool HEAVY = sizeof(T) == 8 && P::NCOEF == 0 && P::NP == P::K * P::K && P::K >= 3;
+  static constexpr int WIDE = (P::NCOEF > 0 || !P::HAS_W) ? 8 : (HEAVY ? 6 : 4);
   template <int CW>
   static void launch_tma(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
                          cudaStream_t s, int fl) {
@@ -65,11 +69,12 @@ struct OpsFor {
   }
   static cudaError_t sweep_tma(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
                                cudaStream_t s, int fl) {
-    if (a.L.cw == 8) {
-      if (WIDE != 8) return cudaErrorNotSupported;
+    if (a.L.cw == WIDE) {
       launch_tma<WIDE>(a, m, g, b, s, fl);
-    } else {
+    } else if (a.L.cw == 4) {
       launch_tma<4>(a, m, g, b, s, fl);
+    } else {
+      return cudaErrorNotSupported;
     }
     return cudaGetLastError();
   }
@@ -82,7 +87,7 @@ struct OpsFor {
   static constexpr int wide_cw() { return WIDE; }
   static int tma_occupancy(int cw, size_t smem) {
     int nb = 0;
-    if (cw == 8 && WIDE == 8)
+    if (cw == WIDE)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_tma_kernel<P, T, 0, WIDE>, 32 * (WIDE + 1),
                                                     smem);
     else

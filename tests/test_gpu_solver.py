@@ -528,6 +528,33 @@ def test_tma_cta_widths_identical(monkeypatch, warps):
 
 
 
+
+@pytest.mark.parametrize("warps", ["4", "6"])
+def test_tma_heavy_complex_widths_identical(monkeypatch, warps):
+    """3x3 complex-Hermitian l1nuc (255-register payload): the 6-warp /
+    2-stage TMA sweep and the 4-warp one give the same bits as the register
+    sweep."""
+    n = 600
+    l0, l1 = synthetic.matrix_blob_fixtures(n)[:2]
+    cfg = pk.SolverConfig(tau=30.0, norm_u="l1nuc", norm_w="l1nuc", tol_gap=1e-300,
+                          tol_feas=1e-300, max_iters=24, check_every=12)
+    outs = []
+    for tma in ("1", "0"):
+        monkeypatch.setenv("OTFX_TMA", tma)
+        monkeypatch.setenv("OTFX_TMA_WARPS", warps)
+        eng = build_engine("matrix", n, cfg, lindblad=pk.default_lindblad3(), complex_path=True)
+        if tma == "1":
+            inf = eng.info()
+            assert inf["tile_cols"] == 31 * int(warps)
+            assert inf["tma_stages"] == (2 if warps == "6" else 4)
+        eng.set_marginals(l0, l1)
+        eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+        outs.append(eng.get_state())
+        eng.close()
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+
+
 # ---------------------------------------------------------------------------
 # on-chip cluster solve (small grids: whole run loop in one cluster launch)
 # against the streamed per-iteration path: same iterates bit for bit, same
