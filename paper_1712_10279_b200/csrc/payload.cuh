@@ -797,13 +797,34 @@ struct HermPolicy {
     } else if (A.norm_u == NORM_L1) {
       soft_entries(x[0], NP, thr);
       soft_entries(x[1], NP, thr);
-    } else {
+    } else if constexpr (K == 2) {
 #pragma unroll
       for (int d = 0; d < 2; ++d) {
         T mr[K][K], mi[K][K];
         unpack_h(x[d], mr, mi);
         herm_nuc_prox<T, K>(mr, mi, thr);
         pack_h(mr, mi, x[d]);
+      }
+    } else {
+      // one rolled loop over the two direction blocks: a single inlined copy
+      // of the eigensolver (K >= 3 unrolls to thousands of instructions; two
+      // copies per prox overflowed the instruction cache -- ncu stall
+      // "no_instructions").  Blocks are selected with compile-time-indexed
+      // selects, so nothing moves to local memory.
+#pragma unroll 1
+      for (int d = 0; d < 2; ++d) {
+        T blk[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) blk[i] = d == 0 ? x[0][i] : x[1][i];
+        T mr[K][K], mi[K][K];
+        unpack_h(blk, mr, mi);
+        herm_nuc_prox<T, K>(mr, mi, thr);
+        pack_h(mr, mi, blk);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          if (d == 0) x[0][i] = blk[i];
+          else x[1][i] = blk[i];
+        }
       }
     }
     if (A.has_eps) {
@@ -908,7 +929,7 @@ struct HermPolicy {
     } else if (A.norm_w == NORM_L1) {
 #pragma unroll
       for (int q = 0; q < LMAX; ++q) soft_entries(&x[q * NWS], NWS, thr);
-    } else {
+    } else if constexpr (K == 2) {
 #pragma unroll
       for (int q = 0; q < LMAX; ++q) {
         if (q < A.ell) {
@@ -917,6 +938,31 @@ struct HermPolicy {
           herm_nuc_prox<T, K>(mr, mi, thr);
           h_to_skew(mr, mi, &x[q * NWS]);
         }
+      }
+    } else {
+      // rolled over the Lindblad blocks for the same reason as prox_u
+      const int nb = A.ell < LMAX ? A.ell : LMAX;
+#pragma unroll 1
+      for (int q = 0; q < nb; ++q) {
+        T blk[NWS];
+#pragma unroll
+        for (int i = 0; i < NWS; ++i) {
+          T v = x[i];
+#pragma unroll
+          for (int s = 1; s < LMAX; ++s)
+            if (q == s) v = x[s * NWS + i];
+          blk[i] = v;
+        }
+        T mr[K][K], mi[K][K];
+        skew_to_h(blk, mr, mi);
+        herm_nuc_prox<T, K>(mr, mi, thr);
+        h_to_skew(mr, mi, blk);
+#pragma unroll
+        for (int s = 0; s < LMAX; ++s)
+          if (q == s) {
+#pragma unroll
+            for (int i = 0; i < NWS; ++i) x[s * NWS + i] = blk[i];
+          }
       }
     }
     if (A.has_eps) {
