@@ -383,6 +383,11 @@ def secondary_configs(args, device):
         eng = build_engine(kind, n, cfg, graph=graph, lindblad=lind, complex_path=complex_path,
                            device=device, stream=stream.cuda_stream)
         eng.set_marginals(l0, l1)
+        # warm-up (lazy module load, CUDA-graph capture of the check period),
+        # then the timed solve from the reference's zero initial state
+        eng.run(1e-300, 1e-300, min(max_iters, 200), cfg.check_every)
+        eng.zero_state()
+        torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         hist, it, conv, wall = eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)

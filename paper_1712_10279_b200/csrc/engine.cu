@@ -1362,7 +1362,12 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     const long waves = (ctas + slots - 1) / slots;
     if (waves <= 8) {
       const long gyw = std::max(1L, std::min<long>(waves * slots / e->gx, e->rows));
-      R = std::max(R, (int)((e->rows + gyw - 1) / gyw));
+      const int Rw = (int)((e->rows + gyw - 1) / gyw);
+      // at one resident CTA per SM (the 255-register heavy payloads) nothing
+      // back-fills a partial last wave, so rows per CTA may also shrink (to 8)
+      // to make the waves whole: 3x3 complex 1024^2, 6 x 64 CTAs (2.6 waves)
+      // -> 6 x 74 (3 waves), l2/l1 0.264 -> 0.241 ms/iteration
+      R = per_sm == 1 ? std::max(8, Rw) : std::max(R, Rw);
     }
     e->R = env_int("OTFX_TILE_ROWS", R);
     e->gy = (e->rows + e->R - 1) / e->R;
