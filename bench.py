@@ -548,9 +548,11 @@ def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn):
         tb.append(time.perf_counter())
         eng.set_marginals(l0, l1)
         tb.append(time.perf_counter())
+        join = eng.prefault_async()  # as solve_vector does (solver._solve)
         eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+        out = join()
         tb.append(time.perf_counter())
-        eng.get_state()
+        eng.get_state(out)
         tb.append(time.perf_counter())
         eng.close()
         tb.append(time.perf_counter())

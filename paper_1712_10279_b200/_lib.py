@@ -60,6 +60,7 @@ SIGNATURES = {
     "otfx_last_error": (C.c_char_p, []),
     "otfx_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "otfx_release_cached_memory": (C.c_int, []),
+    "otfx_host_prefault": (C.c_int, [_P, C.c_size_t]),
     "otfx_engine_create": (C.c_int, [C.POINTER(EngineDesc), C.POINTER(_P)]),
     "otfx_engine_destroy": (C.c_int, [_P]),
     "otfx_engine_get_info": (C.c_int, [_P, C.POINTER(EngineInfo)]),

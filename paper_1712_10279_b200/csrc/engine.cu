@@ -1671,6 +1671,16 @@ int otfx_release_cached_memory(void) {
   API_END
 }
 
+int otfx_host_prefault(void* p, size_t bytes) {
+  API_BEGIN
+  require(p != nullptr || bytes == 0, OTFX_EINVAL, "null buffer");
+  const long pages = long((bytes + 4095) / 4096);
+  volatile char* c = static_cast<volatile char*>(p);
+#pragma omp parallel for schedule(static) if (pages > 256)
+  for (long q = 0; q < pages; ++q) c[size_t(q) * 4096] = 0;
+  API_END
+}
+
 int otfx_device_count(int* count) {
   API_BEGIN
   require(count != nullptr, OTFX_EINVAL, "null pointer");

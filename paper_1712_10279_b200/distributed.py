@@ -109,12 +109,16 @@ def solve_vector_rows(l0_rows, l1_rows, graph, n, cfg: SolverConfig | None = Non
     try:
         m0, m1 = eng.set_marginals(np.asarray(l0_rows), np.asarray(l1_rows))
         _mass_check(m0, m1)
-        history, it, conv, wall = eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters,
-                                          cfg.check_every)
+        join = eng.prefault_async()  # state arrays faulted in during the run
+        try:
+            history, it, conv, wall = eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters,
+                                              cfg.check_every)
+        finally:
+            out = join()
         last = history[-1]
         rep = SolveReport(conv, it, last.primal, history, wall)
         st = _pack_state(eng, it, last.residual, last.primal, last.dual, last.gap_ratio,
-                         last.feas_residual)
+                         last.feas_residual, out)
         return rep, st
     finally:
         eng.close()

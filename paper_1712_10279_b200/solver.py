@@ -19,6 +19,7 @@ stays identical.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -29,6 +30,10 @@ from .errors import UnsupportedNormError, ValidationError
 from .fields import (FluxField, GraphFlux, GridSpec, QuantumFlux, _trusted)
 from .graph import TransportGraph, lambda_max_graph
 from .lindblad import LindbladSet, lambda_max_L
+
+# returned states at least this large are allocated and pre-faulted on a host
+# thread during the run (_solve)
+_PREFAULT_BYTES = 256 << 20
 
 MASS_MISMATCH_TOL = 1e-9
 _TINY = np.finfo(np.float64).tiny
@@ -276,7 +281,10 @@ class CudaEngine:
             w = np.ascontiguousarray(w, dtype=np.float64 if self.kind == "vector" else np.complex128)
         _lib.check(self._lib.otfx_engine_set_state(self._h, _ptr(ux), _ptr(uy), _ptr(w), _ptr(phi)))
 
-    def get_state(self):
+    def alloc_state(self, prefault=False):
+        """Host arrays for get_state (reference shapes and dtypes,
+        S/fields.py:265-289).  prefault=True takes their page faults now
+        (otfx_host_prefault), e.g. from a thread while run() is on the GPU."""
         shape = (self.nrows, self.n) + self._pshape()
         pdt = self._pdtype()
         ux = np.empty(shape, pdt)
@@ -286,6 +294,37 @@ class CudaEngine:
         if self.kind != "scalar":
             w = np.empty((self.nrows, self.n) + self._wshape(),
                          np.float64 if self.kind == "vector" else np.complex128)
+        if prefault:
+            for a in (ux, uy, w, phi):
+                if a is not None:
+                    _lib.check(self._lib.otfx_host_prefault(_ptr(a), a.nbytes))
+        return ux, uy, w, phi
+
+    def state_nbytes(self):
+        cells = self.nrows * self.n
+        per = int(np.prod(self._pshape(), dtype=np.int64)) * np.dtype(self._pdtype()).itemsize
+        wb = 0
+        if self.kind != "scalar":
+            wb = int(np.prod(self._wshape(), dtype=np.int64)) * (8 if self.kind == "vector" else 16)
+        return cells * (3 * per + wb)
+
+    def prefault_async(self):
+        """Start allocating + pre-faulting the state arrays on a host thread
+        (large states only).  Returns a callable that joins and yields the
+        arrays for get_state(out=...), or None."""
+        if self.state_nbytes() < _PREFAULT_BYTES:
+            return lambda: None
+        box = []
+        th = threading.Thread(target=lambda: box.append(self.alloc_state(prefault=True)))
+        th.start()
+
+        def join():
+            th.join()
+            return box[0] if box else None
+        return join
+
+    def get_state(self, out=None):
+        ux, uy, w, phi = out if out is not None else self.alloc_state()
         _lib.check(self._lib.otfx_engine_get_state(self._h, _ptr(ux), _ptr(uy), _ptr(w), _ptr(phi)))
         return ux, uy, w, phi
 
@@ -447,8 +486,8 @@ def build_engine(kind, n, cfg, graph=None, lindblad=None, precision="f64", devic
     return CudaEngine(kname, n, mu=mu, nu=nu, k=lindblad.k, ell=lindblad.ell, chan=chan, **common)
 
 
-def _pack_state(engine, it, rk, primal, dual, gap, feas):
-    ux, uy, w, phi = engine.get_state()
+def _pack_state(engine, it, rk, primal, dual, gap, feas, out=None):
+    ux, uy, w, phi = engine.get_state(out)
     if engine.kind == "scalar":
         wobj = None
     elif engine.kind == "vector":
@@ -464,12 +503,19 @@ def _solve(engine, l0v, l1v, cfg):
     try:
         m0, m1 = engine.set_marginals(l0v, l1v)
         _mass_check(m0, m1)
-        history, it, conv, wall = engine.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters,
-                                             cfg.check_every)
+        # large states: the returned arrays are allocated and their page faults
+        # taken on a host thread while the run occupies the GPU (the ctypes call
+        # releases the GIL), so the download is bound by the copies alone
+        join = engine.prefault_async()
+        try:
+            history, it, conv, wall = engine.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters,
+                                                 cfg.check_every)
+        finally:
+            out = join()
         last = history[-1]
         report = SolveReport(conv, it, last.primal, history, wall)
         state = _pack_state(engine, it, last.residual, last.primal, last.dual, last.gap_ratio,
-                            last.feas_residual)
+                            last.feas_residual, out)
         return report, state
     finally:
         engine.close()

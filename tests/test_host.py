@@ -179,3 +179,17 @@ def test_bench_reference_arm_contract():
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env,
                          check=True)
     assert out.stdout.strip() == ""
+
+
+def test_host_prefault_touches_buffer_without_gpu():
+    """otfx_host_prefault is host-only (no device call): it writes one zero
+    per 4 KiB page of the buffer and leaves a null/empty request alone."""
+    lib = _lib.load()
+    a = np.full(3 * 4096 // 8 + 5, 7.0)
+    _lib.check(lib.otfx_host_prefault(a.ctypes.data, a.nbytes))
+    b = a.view(np.uint8)
+    assert b[0] == 0 and b[4096] == 0 and b[8192] == 0
+    assert b[1] == np.float64(7.0).tobytes()[1]
+    _lib.check(lib.otfx_host_prefault(None, 0))
+    with pytest.raises(pk.ValidationError):
+        _lib.check(lib.otfx_host_prefault(None, 8))
