@@ -12,7 +12,9 @@ import paper_1712_10279_b200 as pk
 from paper_1712_10279_b200 import synthetic
 from paper_1712_10279_b200.solver import build_engine
 out = {}
-for n, iters in ((48, 2000), (64, 2000), (80, 2000), (128, 2000)):
+import os
+sizes = [int(x) for x in os.environ.get("SIZES", "48,64,80,128").split(",")]
+for n, iters in ((m, 2000) for m in sizes):
     l0, l1 = synthetic.rgb_disk_pair(n)
     cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", tol_gap=1e-300, tol_feas=1e-300,
                           max_iters=iters, check_every=100)
@@ -28,7 +30,9 @@ for n, iters in ((48, 2000), (64, 2000), (80, 2000), (128, 2000)):
     eng.close()
 print(json.dumps(out))
 '''
-for env in [{}, {"OTFX_CLUSTER_CTAS": "8"}, {"OTFX_CLUSTER": "0"}]:
+variants = [json.loads(a) for a in sys.argv[1:]] or [{}, {"OTFX_CLUSTER_CTAS": "8"},
+                                                      {"OTFX_CLUSTER": "0"}]
+for env in variants:
     e = dict(os.environ)
     e.update(env)
     r = subprocess.run([sys.executable, "-c", SNIP], env=e, capture_output=True, text=True,
