@@ -236,9 +236,11 @@ __device__ __forceinline__ cpx<T> cmul(cpx<T> a, cpx<T> b) {
 template <typename T>
 __device__ __forceinline__ cpx<T> cadd(cpx<T> a, cpx<T> b) { return {a.r + b.r, a.i + b.i}; }
 // acc + a*b with fused multiply-adds (4 FMA instead of 4 MUL + 4 ADD).  The
-// library is built with --fmad=false so the vector/scalar/real paths round
-// exactly like the NumPy reference; only the K >= 3 complex-Hermitian payload
-// (whose eigensolver differs from LAPACK anyway; parity 1e-10) opts in here.
+// library is built with --fmad=false so the vector and scalar paths round
+// exactly like the NumPy reference (bit-identical iterates); the matrix
+// payloads, whose reference runs einsum / LAPACK with their own summation
+// orders (parity 1e-10), opt in for the Lindblad commutators and the
+// eigensolver.
 template <typename T>
 __device__ __forceinline__ cpx<T> cmac(cpx<T> acc, cpx<T> a, cpx<T> b) {
   return {fma(a.r, b.r, fma(-a.i, b.i, acc.r)), fma(a.r, b.i, fma(a.i, b.r, acc.i))};
@@ -545,7 +547,7 @@ struct SymPolicy {
         for (int b = 0; b < K; ++b) {
           T acc = T(0);
 #pragma unroll
-          for (int c = 0; c < K; ++c) acc = acc + L(A, s, a, c) * X[c][b];
+          for (int c = 0; c < K; ++c) acc = fma(L(A, s, a, c), X[c][b], acc);
           P[a][b] = acc;
         }
 #pragma unroll
@@ -581,7 +583,7 @@ struct SymPolicy {
         for (int b = 0; b < K; ++b) {
           T acc = Tm[a][b];
 #pragma unroll
-          for (int c = 0; c < K; ++c) acc = acc + Z[a][c] * L(A, s, c, b);
+          for (int c = 0; c < K; ++c) acc = fma(Z[a][c], L(A, s, c, b), acc);
           Tm[a][b] = acc;
         }
     }
@@ -863,10 +865,7 @@ struct HermPolicy {
         for (int b = 0; b < K; ++b) {
           cpx<T> acc = {T(0), T(0)};
 #pragma unroll
-          for (int c = 0; c < K; ++c) {
-            if constexpr (K >= 3) acc = cmac(acc, L(A, s, a, c), cpx<T>{xr[c][b], xi[c][b]});
-            else acc = cadd(acc, cmul(L(A, s, a, c), cpx<T>{xr[c][b], xi[c][b]}));
-          }
+          for (int c = 0; c < K; ++c) acc = cmac(acc, L(A, s, a, c), cpx<T>{xr[c][b], xi[c][b]});
           P[a][b] = acc;
         }
       T* z = &g[s * NWS];
@@ -911,10 +910,7 @@ struct HermPolicy {
         for (int b = 0; b < K; ++b) {
           cpx<T> acc = Tm[a][b];
 #pragma unroll
-          for (int c = 0; c < K; ++c) {
-            if constexpr (K >= 3) acc = cmac(acc, Z[a][c], L(A, s, c, b));
-            else acc = cadd(acc, cmul(Z[a][c], L(A, s, c, b)));
-          }
+          for (int c = 0; c < K; ++c) acc = cmac(acc, Z[a][c], L(A, s, c, b));
           Tm[a][b] = acc;
         }
     }
