@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--ref-n", type=int, default=2048, help="CPU sample grid side")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--ref-seconds", type=float, default=75.0,
+                   help="bound on the timed sample of the reference arm")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-secondary", action="store_true",
@@ -163,44 +165,101 @@ def cpu_baseline(ref_n, seconds, max_steps=None):
                        f"BLAS pool = {cores} threads")
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _import_reference():
+    """The unmodified reference package (otflux) installed into baseline/_ref
+    (DESIGN.md §10); None when it is absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "otflux")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import otflux  # noqa: F401
+        from otflux import solver as ref_solver
+    except Exception:
+        return None
+    return otflux, ref_solver
+
+
 def run_reference(args):
+    """The reference's own CPU engine on the bench workload: otflux's
+    ``_engine_for("vector", ...)`` (S/solver.py:450-464) stepped with
+    ``_Engine.step()`` (S/solver.py:220-240) at the grid our arm runs per GPU
+    (8192^2 rgb_disk_pair from the reference's own generator,
+    S/problems.py:175-185), BLAS pool = all host cores.  One reference step at
+    8192^2 takes ~30 s, so the timed sample is bounded by --ref-seconds
+    (at least 2 steps, at most --steps) after one warm-up step; the line says
+    how many steps were timed.  Falls back to the NumPy port (oracle/) at
+    --ref-n when baseline/_ref is missing."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from threadpoolctl import threadpool_limits
 
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    n = global_n(args.n, world)
+    cores = os.cpu_count() or 1
+    ref = _import_reference()
+    if ref is not None:
+        otflux, ref_solver = ref
+        n_ref = args.n
+        l0, l1 = otflux.rgb_disk_pair(otflux.GridSpec(n_ref))
+        cfg = otflux.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", alpha=1.0,
+                                  check_every=args.iters_per_step)
+        kind = "reference"
+        with threadpool_limits(limits=cores):
+            eng = ref_solver._engine_for("vector", l0, l1, cfg, graph=otflux.triangle_graph())
+            del l0, l1
+            step = eng.step
+            what = (f"otflux (baseline/_ref, unmodified) _Engine.step() at {n_ref}^2, "
+                    f"{cores} BLAS threads")
+            _time_reference(args, step, n_ref, n, world, cores, kind, what)
+        return
     from oracle.pdhg import OracleEngine, graph_coef
     import paper_1712_10279_b200 as pk
     from paper_1712_10279_b200 import synthetic
 
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     n_ref = args.ref_n
     l0, l1 = synthetic.rgb_disk_pair(n_ref)
     g = pk.triangle_graph()
-    cores = os.cpu_count() or 1
     with threadpool_limits(limits=cores):
         eng = OracleEngine("vector", l0 - l1, n_ref, 6.0, norm_u="l12", norm_w="l1", alpha=1.0,
                            chan=graph_coef(3, g.edges, g.costs), lam_chan=pk.lambda_max_graph(g))
-        for _ in range(args.warmup):
-            eng.step()
+        what = (f"NumPy port of the reference engine (oracle/, baseline/_ref missing) at "
+                f"{n_ref}^2, {cores} BLAS threads")
+        _time_reference(args, eng.step, n_ref, n, world, cores, "port", what)
+
+
+def _time_reference(args, step, n_ref, n, world, cores, kind, what):
+    step()  # warm-up: first-touch page faults of the iterate arrays
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max(1, args.steps):
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            eng.step()
-        el = time.perf_counter() - t0
-    value = n_ref * n_ref * args.steps / el
-    n = global_n(args.n, world)
+        step()
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 2 and time.perf_counter() - t_all >= args.ref_seconds:
+            break
+    el = float(sum(times))
+    steps = len(times)
+    value = n_ref * n_ref * steps / el
+    sample = (f"{steps} timed PDHG iterations (+1 warm-up) of {what}; "
+              f"{el:.1f} s, {1e3 * el / steps:.0f} ms/iteration")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "steps": steps, "warmup": 1, "ms_per_step": 1e3 * el / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference rgb_disk_pair generator (deterministic)",
-        "config": {"workload": f"BASELINE configs[4] vector-OMT 3-channel, n={n} (sampled on the "
-                               f"host at {n_ref}^2, one PDHG iteration per step)",
-                   "n": n, "sample_n": n_ref, "k": K_CH, "ell": ELL, "norms": "l12/l1",
-                   "tau": 6.0, "alpha": 1.0},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} iterations of the NumPy port of the reference "
-                                   f"engine at {n_ref}^2 after {args.warmup} warm-up iterations"},
+        "config": {"workload": f"BASELINE configs[4] vector-OMT 3-channel, {n_ref}^2 on the "
+                               f"host (our arm: n={n} global over {world} GPU(s)); one "
+                               f"reference step = one PDHG iteration",
+                   "n": n, "sample_n": n_ref, "same_config": n_ref == n, "k": K_CH, "ell": ELL,
+                   "norms": "l12/l1", "tau": 6.0, "alpha": 1.0,
+                   "steps_requested": args.steps, "warmup_requested": args.warmup},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -141,6 +141,24 @@ int otfx_engine_set_marginals(otfx_engine* e, const double* l0, const double* l1
  * float64 (rows,n,k,k); complex path: complex128) */
 int otfx_engine_set_diff(otfx_engine* e, const double* diff);
 
+/* Device-pointer hand-off (SURVEY §8(b) ownership row: torch owns the
+ * tensors, the library reads / writes them in place and keeps no reference).
+ * Same layouts and dtypes as the host calls, arrays resident on the engine's
+ * device (e.g. torch.Tensor.data_ptr() of a contiguous float64 / complex128
+ * CUDA tensor).  `stream` is the caller's cudaStream_t (NULL = legacy default
+ * stream): the engine's work is ordered after the caller's prior work on it,
+ * and the caller's later work after the engine's reads / writes (CUDA events,
+ * no host synchronisation; set_marginals_device synchronises once to return
+ * the masses and ||diff||).  Replace the host-array versions of
+ * _Engine.__init__'s diff (S/solver.py:179-185), _load_state
+ * (S/solver.py:477-482) and the state packing (S/solver.py:318-336). */
+int otfx_engine_set_marginals_device(otfx_engine* e, const double* l0, const double* l1,
+                                     double masses[2], void* stream);
+int otfx_engine_set_state_device(otfx_engine* e, const double* ux, const double* uy,
+                                 const double* w, const double* phi, void* stream);
+int otfx_engine_get_state_device(otfx_engine* e, double* ux, double* uy, double* w, double* phi,
+                                 void* stream);
+
 /* ||diff|| used by the feasibility residual (S/solver.py:185, 246): read the
  * engine's value (its own rows, or the global one under NCCL) and/or
  * override it (local multi-slab drivers combine the slabs' values) */

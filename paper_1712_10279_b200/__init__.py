@@ -14,7 +14,7 @@ from .graph import TransportGraph, lambda_max_graph, triangle_graph
 from .lindblad import LindbladSet, default_lindblad3, lambda_max_L, lindblad_pair_k2
 from .solver import (CudaEngine, HistoryPoint, NormFamily, SolveReport, SolverConfig, SolverState,
                      default_tau, duality_gap, residual_Rk, solve_matrix, solve_scalar,
-                     solve_vector, step_sizes_matrix, step_sizes_scalar, step_sizes_vector)
+                     solve_tensors, solve_vector, step_sizes_matrix, step_sizes_scalar, step_sizes_vector)
 
 from ._lib import release_cached_memory
 

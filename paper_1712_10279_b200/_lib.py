@@ -65,6 +65,9 @@ SIGNATURES = {
     "otfx_engine_destroy": (C.c_int, [_P]),
     "otfx_engine_get_info": (C.c_int, [_P, C.POINTER(EngineInfo)]),
     "otfx_engine_set_marginals": (C.c_int, [_P, _P, _P, _DP]),
+    "otfx_engine_set_marginals_device": (C.c_int, [_P, _P, _P, _DP, _P]),
+    "otfx_engine_set_state_device": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+    "otfx_engine_get_state_device": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "otfx_engine_set_diff": (C.c_int, [_P, _P]),
     "otfx_engine_diff_norm": (C.c_int, [_P, _DP, _DP]),
     "otfx_engine_zero_state": (C.c_int, [_P]),

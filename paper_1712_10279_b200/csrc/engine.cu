@@ -316,6 +316,7 @@ struct otfx_engine {
   // overlapped halo exchange: edge bands + exchange on a high-priority stream
   cudaStream_t edge_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_hand = nullptr;  // caller-stream ordering of the device hand-off
   // TMA-streamed sweep
   bool use_tma = false;
   otfx::StageLayout L{};
@@ -1065,18 +1066,31 @@ static void pack_chunk(otfx_engine* e, const double* s0, const double* s1, int64
 // ---- pinned staging pool shared by all engines of the process -------------
 // Host <-> device transfers go through two pinned slots per direction so the
 // multi-threaded host memcpy of chunk k overlaps the DMA of chunk k-1.
+// The slot-reuse events are recorded on the engine's stream, so they are
+// created per device (an event recorded on another device's stream is an
+// error): ev_of(device) is called with the pool lock held and the engine's
+// device current.
 struct PinnedPool {
   static constexpr size_t kSlot = size_t(32) << 20;  // bytes per slot
   unsigned char* buf = nullptr;                        // 4 slots: 2 x (in0, in1)
-  cudaEvent_t ev[2]{};
+  std::map<int, std::pair<cudaEvent_t, cudaEvent_t>> ev;
   std::mutex mu;
+  cudaEvent_t* ev_of(int device) {
+    auto it = ev.find(device);
+    if (it == ev.end()) {
+      std::pair<cudaEvent_t, cudaEvent_t> pr{};
+      CK(cudaEventCreateWithFlags(&pr.first, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&pr.second, cudaEventDisableTiming));
+      it = ev.emplace(device, pr).first;
+    }
+    return &it->second.first;
+  }
 };
 
 static PinnedPool& pinned_pool() {
   static PinnedPool* p = [] {
     PinnedPool* q = new PinnedPool();
     CK(cudaMallocHost(&q->buf, 4 * PinnedPool::kSlot));
-    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&q->ev[i], cudaEventDisableTiming));
     return q;
   }();
   return *p;
@@ -1102,6 +1116,7 @@ static void host_to_planes(otfx_engine* e, const double* h0, const double* h1, c
                            void* planes, double sums[3]) {
   PinnedPool& P = pinned_pool();
   std::lock_guard<std::mutex> lock(P.mu);
+  cudaEvent_t ev[2] = {P.ev_of(e->d.device)[0], P.ev_of(e->d.device)[1]};
   const int n = e->d.n;
   const size_t row_bytes = size_t(n) * m.rec * sizeof(double);
   const size_t slot = std::min(PinnedPool::kSlot, e->stage_bytes / 4);
@@ -1123,12 +1138,12 @@ static void host_to_planes(otfx_engine* e, const double* h0, const double* h1, c
     unsigned char* pin1 = pin0 + PinnedPool::kSlot;
     double* st0 = e->d_stage + size_t(b) * (e->stage_bytes / 2 / sizeof(double));
     double* st1 = st0 + slot / sizeof(double);
-    if (k >= 2) CK(cudaEventSynchronize(P.ev[b]));  // slot b free again
+    if (k >= 2) CK(cudaEventSynchronize(ev[b]));  // slot b free again
     par_copy(pin0, h0 + off, bytes);
     if (h1) par_copy(pin1, h1 + off, bytes);
     CK(cudaMemcpyAsync(st0, pin0, bytes, cudaMemcpyHostToDevice, e->stream));
     if (h1) CK(cudaMemcpyAsync(st1, pin1, bytes, cudaMemcpyHostToDevice, e->stream));
-    CK(cudaEventRecord(P.ev[b], e->stream));
+    CK(cudaEventRecord(ev[b], e->stream));
     if (e->elem == 8) pack_chunk<double>(e, st0, h1 ? st1 : nullptr, int64_t(nr) * n, planes, 1 + r0, m);
     else pack_chunk<float>(e, st0, h1 ? st1 : nullptr, int64_t(nr) * n, planes, 1 + r0, m);
     CK(cudaMemcpyAsync(hp + size_t(k) * kPackBlocks * 3, e->d_pack_part,
@@ -1147,6 +1162,7 @@ static void host_to_planes(otfx_engine* e, const double* h0, const double* h1, c
 static void planes_to_host(otfx_engine* e, const void* planes, const UnpackMap& m, double* h) {
   PinnedPool& P = pinned_pool();
   std::lock_guard<std::mutex> lock(P.mu);
+  cudaEvent_t ev[2] = {P.ev_of(e->d.device)[0], P.ev_of(e->d.device)[1]};
   const int n = e->d.n;
   const size_t row_bytes = size_t(n) * m.rec * sizeof(double);
   const size_t slot = std::min(PinnedPool::kSlot, e->stage_bytes / 4);
@@ -1170,18 +1186,66 @@ static void planes_to_host(otfx_engine* e, const void* planes, const UnpackMap& 
           static_cast<const float*>(planes), e->plane, e->pitch, 1 + r0, ncell, n, m, st);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(pin, st, size_t(nr) * row_bytes, cudaMemcpyDeviceToHost, e->stream));
-    CK(cudaEventRecord(P.ev[b], e->stream));
+    CK(cudaEventRecord(ev[b], e->stream));
   };
   launch(0);
   for (int k = 0; k < nchunks; ++k) {
     if (k + 1 < nchunks) launch(k + 1);  // next chunk's DMA overlaps this chunk's memcpy
     const int b = k & 1;
-    CK(cudaEventSynchronize(P.ev[b]));
+    CK(cudaEventSynchronize(ev[b]));
     const int r0 = k * chunk;
     const int nr = std::min(chunk, e->rows - r0);
     par_copy(h + size_t(r0) * n * m.rec, P.buf + size_t(2 * b) * PinnedPool::kSlot,
              size_t(nr) * row_bytes);
   }
+}
+
+// ---- device-pointer hand-off (torch-owned tensors) ----------
+// The caller's arrays live on the engine's device in the reference layout;
+// they are read / written in place by the pack / unpack kernels, ordered
+// against the caller's stream with events (no host synchronisation unless a
+// host-side scalar is needed).
+static void stream_wait(cudaStream_t waiter, cudaStream_t on, cudaEvent_t ev) {
+  if (waiter == on) return;
+  CK(cudaEventRecord(ev, on));
+  CK(cudaStreamWaitEvent(waiter, ev, 0));
+}
+
+static void check_device_ptr(const otfx_engine* e, const void* p) {
+  if (!p) return;
+  cudaPointerAttributes a{};
+  CK(cudaPointerGetAttributes(&a, p));
+  require(a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged, OTFX_EINVAL,
+          "expected a device pointer");
+  require(a.device == e->d.device, OTFX_EINVAL, "device pointer on another device");
+}
+
+static void device_to_planes(otfx_engine* e, const double* d0, const double* d1, const PackMap& m,
+                             void* planes, double sums[3]) {
+  const int64_t ncell = int64_t(e->rows) * e->d.n;
+  if (e->elem == 8) pack_chunk<double>(e, d0, d1, ncell, planes, 1, m);
+  else pack_chunk<float>(e, d0, d1, ncell, planes, 1, m);
+  if (!sums) return;
+  CK(cudaMemcpyAsync(e->h_pack_part, e->d_pack_part, kPackBlocks * 3 * sizeof(double),
+                     cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  sums[0] = sums[1] = sums[2] = 0.0;
+  for (int q = 0; q < kPackBlocks * 3; q += 3) {
+    sums[0] += e->h_pack_part[q];
+    sums[1] += e->h_pack_part[q + 1];
+    sums[2] += e->h_pack_part[q + 2];
+  }
+}
+
+static void planes_to_device(otfx_engine* e, const void* planes, const UnpackMap& m, double* d) {
+  const int64_t ncell = int64_t(e->rows) * e->d.n;
+  if (e->elem == 8)
+    unpack_kernel<double><<<kPackBlocks, 256, 0, e->stream>>>(
+        static_cast<const double*>(planes), e->plane, e->pitch, 1, ncell, e->d.n, m, d);
+  else
+    unpack_kernel<float><<<kPackBlocks, 256, 0, e->stream>>>(
+        static_cast<const float*>(planes), e->plane, e->pitch, 1, ncell, e->d.n, m, d);
+  CK(cudaGetLastError());
 }
 
 static void* plane_ptr(otfx_engine* e, void* base, int p) {
@@ -1473,6 +1537,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   }
   CK(cudaMallocHost(&e->h_raw, 64 * sizeof(double)));
   CK(cudaMallocHost(&e->h_pack_part, kPackBlocks * 3 * sizeof(double)));
+  CK(cudaEventCreateWithFlags(&e->ev_hand, cudaEventDisableTiming));
   CK(e->ops64 ? e->ops64->prepare() : e->ops32->prepare());
   e->use_graphs = env_int("OTFX_GRAPHS", 1) != 0;
   CK(cudaStreamSynchronize(e->stream));
@@ -1492,6 +1557,7 @@ static void destroy(otfx_engine* e) {
   }
   if (e->ev_fork) cudaEventDestroy(e->ev_fork);
   if (e->ev_join) cudaEventDestroy(e->ev_join);
+  if (e->ev_hand) cudaEventDestroy(e->ev_hand);
   if (e->comm && e->own_comm && nccl().CommDestroy) nccl().CommDestroy(e->comm);
   if (e->mem) {
     if (e->pooled) {
@@ -1748,24 +1814,85 @@ int otfx_engine_get_info(otfx_engine* e, otfx_engine_info* info) {
   API_END
 }
 
-int otfx_engine_set_marginals(otfx_engine* e, const double* l0, const double* l1, double masses[2]) {
-  API_BEGIN
-  require(e && l0 && l1, OTFX_EINVAL, "null pointer");
-  CK(cudaSetDevice(e->d.device));
+static PackMap marginals_map(const otfx_engine* e) {
   PackMap m = potential_pack(e, e->d.kind >= OTFX_KIND_MATRIX_REAL);
   if (e->d.kind == OTFX_KIND_VECTOR) {
     for (int c = 0; c < e->K; ++c) add_mass(m, c);
   } else if (e->d.kind >= OTFX_KIND_MATRIX_REAL) {
     for (int a = 0; a < e->K; ++a) add_mass(m, 2 * (a * e->K + a));
   }
-  double sums[3];
-  host_to_planes(e, l0, l1, m, e->diff, sums);
+  return m;
+}
+
+static void take_marginal_sums(otfx_engine* e, double sums[3], double masses[2]) {
   allreduce_host(e, sums, 3);
   e->diff_norm = std::sqrt(sums[2]);
   if (masses) {
     masses[0] = sums[0];
     masses[1] = sums[1];
   }
+}
+
+int otfx_engine_set_marginals(otfx_engine* e, const double* l0, const double* l1, double masses[2]) {
+  API_BEGIN
+  require(e && l0 && l1, OTFX_EINVAL, "null pointer");
+  CK(cudaSetDevice(e->d.device));
+  double sums[3];
+  host_to_planes(e, l0, l1, marginals_map(e), e->diff, sums);
+  take_marginal_sums(e, sums, masses);
+  API_END
+}
+
+int otfx_engine_set_marginals_device(otfx_engine* e, const double* l0, const double* l1,
+                                     double masses[2], void* stream) {
+  API_BEGIN
+  require(e && l0 && l1, OTFX_EINVAL, "null pointer");
+  CK(cudaSetDevice(e->d.device));
+  check_device_ptr(e, l0);
+  check_device_ptr(e, l1);
+  stream_wait(e->stream, static_cast<cudaStream_t>(stream), e->ev_hand);
+  double sums[3];
+  device_to_planes(e, l0, l1, marginals_map(e), e->diff, sums);  // synchronises e->stream
+  take_marginal_sums(e, sums, masses);
+  API_END
+}
+
+int otfx_engine_set_state_device(otfx_engine* e, const double* ux, const double* uy,
+                                 const double* w, const double* phi, void* stream) {
+  API_BEGIN
+  require(e && ux && uy && phi, OTFX_EINVAL, "null pointer");
+  require(!e->has_w || w, OTFX_EINVAL, "channel flux missing");
+  CK(cudaSetDevice(e->d.device));
+  for (const double* p : {ux, uy, w, phi}) check_device_ptr(e, p);
+  zero_state(e);
+  const cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  stream_wait(e->stream, caller, e->ev_hand);
+  const int c = e->cur;
+  PackMap pm = potential_pack(e, e->d.kind == OTFX_KIND_MATRIX_COMPLEX);
+  device_to_planes(e, ux, nullptr, pm, e->u[c], nullptr);
+  device_to_planes(e, uy, nullptr, pm, plane_ptr(e, e->u[c], e->NP), nullptr);
+  device_to_planes(e, phi, nullptr, pm, e->phi[c], nullptr);
+  if (e->has_w) device_to_planes(e, w, nullptr, flux_w_pack(e), e->w[c], nullptr);
+  exchange_nccl(e);
+  stream_wait(caller, e->stream, e->ev_hand);
+  API_END
+}
+
+int otfx_engine_get_state_device(otfx_engine* e, double* ux, double* uy, double* w, double* phi,
+                                 void* stream) {
+  API_BEGIN
+  require(e, OTFX_EINVAL, "null engine");
+  CK(cudaSetDevice(e->d.device));
+  for (const double* p : {ux, uy, w, phi}) check_device_ptr(e, p);
+  const cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  stream_wait(e->stream, caller, e->ev_hand);
+  const int c = e->cur;
+  UnpackMap pm = potential_unpack(e);
+  if (ux) planes_to_device(e, e->u[c], pm, ux);
+  if (uy) planes_to_device(e, plane_ptr(e, e->u[c], e->NP), pm, uy);
+  if (phi) planes_to_device(e, e->phi[c], pm, phi);
+  if (w && e->has_w) planes_to_device(e, e->w[c], flux_w_unpack(e), w);
+  stream_wait(caller, e->stream, e->ev_hand);
   API_END
 }
 

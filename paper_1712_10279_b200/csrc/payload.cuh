@@ -88,26 +88,38 @@ struct VecPolicy {
     }
   }
 
-  // graph gradient diag(1/c) D^T phi  (S/graph.py:105-114)
+  // graph gradient diag(1/c) D^T phi  (S/graph.py:105-114).  The reference
+  // computes it as the matmul (n^2, k) @ (k, ell), which NumPy hands to
+  // OpenBLAS: dgemm accumulates every output with a fused multiply-add chain
+  // over k in ascending order from 0, and for ell = 1 (k = 2, a single edge)
+  // the matrix-vector kernel runs the chain in descending order
+  // (tools/blas_order.py checks both against NumPy).  The same chains here
+  // make the channel update bit-identical to the reference.
   template <class PA>
   __device__ static void grad_c(const T (&p)[NP], T (&g)[NWA], const PA& A) {
 #pragma unroll
     for (int e = 0; e < NWA; ++e) {
       T s = T(0);
+      if constexpr (K == 2) {
+        s = fma(p[1], T(A.coef[1 * LMAX + e]), s);
+        s = fma(p[0], T(A.coef[0 * LMAX + e]), s);
+      } else {
 #pragma unroll
-      for (int c = 0; c < K; ++c) s = s + p[c] * T(A.coef[c * LMAX + e]);
+        for (int c = 0; c < K; ++c) s = fma(p[c], T(A.coef[c * LMAX + e]), s);
+      }
       g[e] = s;
     }
   }
 
-  // graph divergence -D diag(1/c) y  (S/graph.py:117-123)
+  // graph divergence -D diag(1/c) y  (S/graph.py:117-123): the matmul
+  // (n^2, ell) @ (ell, k), an ascending fused multiply-add chain over ell
   template <class PA>
   __device__ static void div_c(const T (&y)[NWA], T (&d)[NP], const PA& A) {
 #pragma unroll
     for (int c = 0; c < K; ++c) {
       T s = T(0);
 #pragma unroll
-      for (int e = 0; e < NWA; ++e) s = s + y[e] * T(-A.coef[c * LMAX + e]);
+      for (int e = 0; e < NWA; ++e) s = fma(y[e], T(-A.coef[c * LMAX + e]), s);
       d[c] = s;
     }
   }

@@ -328,6 +328,72 @@ class CudaEngine:
         _lib.check(self._lib.otfx_engine_get_state(self._h, _ptr(ux), _ptr(uy), _ptr(w), _ptr(phi)))
         return ux, uy, w, phi
 
+    # -- device-pointer hand-off (torch CUDA tensors) --------------------------
+    def _torch_stream(self, stream):
+        import torch
+
+        if stream is None:
+            stream = torch.cuda.current_stream(self._desc.device)
+        return C.c_void_p(stream.cuda_stream)
+
+    def _tensor_ptr(self, t, dtype):
+        """data_ptr of a contiguous CUDA tensor of the engine's device in the
+        reference layout (complex128 tensors are interleaved doubles)."""
+        import torch
+
+        if t is None:
+            return None
+        want = torch.complex128 if dtype == np.complex128 else torch.float64
+        if not (t.is_cuda and t.dtype == want and t.is_contiguous()
+                and t.device.index == self._desc.device):
+            raise ValidationError(
+                f"expected a contiguous {want} tensor on cuda:{self._desc.device}, got "
+                f"{t.dtype} on {t.device} (contiguous={t.is_contiguous()})")
+        return C.c_void_p(t.data_ptr())
+
+    def set_marginals_device(self, l0, l1, stream=None):
+        """set_marginals for torch CUDA tensors (read in place on the device)."""
+        dt = np.complex128 if self.kind.startswith("matrix") else np.float64
+        m = (C.c_double * 2)()
+        _lib.check(self._lib.otfx_engine_set_marginals_device(
+            self._h, self._tensor_ptr(l0, dt), self._tensor_ptr(l1, dt), m,
+            self._torch_stream(stream)))
+        return m[0], m[1]
+
+    def set_state_device(self, ux, uy, w, phi, stream=None):
+        pdt = self._pdtype()
+        wdt = np.float64 if self.kind == "vector" else np.complex128
+        _lib.check(self._lib.otfx_engine_set_state_device(
+            self._h, self._tensor_ptr(ux, pdt), self._tensor_ptr(uy, pdt),
+            self._tensor_ptr(w, wdt), self._tensor_ptr(phi, pdt), self._torch_stream(stream)))
+
+    def alloc_state_device(self):
+        """torch CUDA tensors for get_state_device (reference shapes / dtypes)."""
+        import torch
+
+        dev = torch.device("cuda", self._desc.device)
+        shape = (self.nrows, self.n) + self._pshape()
+        pdt = torch.complex128 if self._pdtype() == np.complex128 else torch.float64
+        ux = torch.empty(shape, dtype=pdt, device=dev)
+        uy = torch.empty_like(ux)
+        phi = torch.empty_like(ux)
+        w = None
+        if self.kind != "scalar":
+            wdt = torch.float64 if self.kind == "vector" else torch.complex128
+            w = torch.empty((self.nrows, self.n) + self._wshape(), dtype=wdt, device=dev)
+        return ux, uy, w, phi
+
+    def get_state_device(self, out=None, stream=None):
+        """The current iterate written into torch CUDA tensors on the caller's
+        stream order (no host round trip)."""
+        ux, uy, w, phi = out if out is not None else self.alloc_state_device()
+        pdt = self._pdtype()
+        wdt = np.float64 if self.kind == "vector" else np.complex128
+        _lib.check(self._lib.otfx_engine_get_state_device(
+            self._h, self._tensor_ptr(ux, pdt), self._tensor_ptr(uy, pdt),
+            self._tensor_ptr(w, wdt), self._tensor_ptr(phi, pdt), self._torch_stream(stream)))
+        return ux, uy, w, phi
+
     # -- iteration ------------------------------------------------------------
     def step(self, iters=1):
         _lib.check(self._lib.otfx_engine_step(self._h, int(iters)))
@@ -569,6 +635,85 @@ def solve_matrix(Lambda0, Lambda1, lindblad: LindbladSet, grid: GridSpec | None 
     eng = build_engine("matrix", grid.n, cfg, lindblad=lindblad, precision=precision,
                        device=device, complex_path=not use_real)
     return _solve(eng, l0v, l1v, cfg)
+
+
+def solve_tensors(lambda0, lambda1, channels=None, cfg: SolverConfig | None = None, *,
+                  precision="f64"):
+    """``solve_scalar`` / ``solve_vector`` / ``solve_matrix`` for marginals
+    already resident on a GPU as torch tensors (SURVEY §8(b) ownership row:
+    torch owns the tensors, the engine reads them in place).
+
+    The kind follows the tensor rank, as the reference's density types do
+    (S/fields.py:183-229): (n, n) scalar, (n, n, k) vector with ``channels`` a
+    TransportGraph, (n, n, k, k) matrix with ``channels`` a LindbladSet.
+    Validation, step sizes, the real/complex matrix rule (S/solver.py:412-419)
+    and the run loop are those of the host entry points; the returned
+    SolverState holds torch tensors on the marginals' device (same shapes and
+    dtypes as the NumPy arrays of the host path), written by the engine
+    without a host round trip."""
+    import torch
+
+    cfg = cfg if cfg is not None else SolverConfig()
+    for t in (lambda0, lambda1):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda):
+            raise ValidationError("solve_tensors expects torch CUDA tensors")
+    if lambda0.shape != lambda1.shape:
+        raise ValidationError(f"marginal shapes differ: {tuple(lambda0.shape)} vs "
+                              f"{tuple(lambda1.shape)}")
+    if lambda0.device != lambda1.device:
+        raise ValidationError("marginals on different devices")
+    nd = lambda0.dim()
+    if nd < 2 or lambda0.shape[0] != lambda0.shape[1]:
+        raise ValidationError(f"expected a square grid, got shape {tuple(lambda0.shape)}")
+    n = lambda0.shape[0]
+    device = lambda0.device.index or 0
+    _reject_regularized_nuclear(cfg)
+    if nd == 2:
+        validate_norm(cfg.norm_u, "scalar", "u")
+        eng = build_engine("scalar", n, cfg, precision=precision, device=device)
+        a, b = lambda0.to(torch.float64).contiguous(), lambda1.to(torch.float64).contiguous()
+    elif nd == 3:
+        if not isinstance(channels, TransportGraph) or channels.k != lambda0.shape[2]:
+            raise ValidationError("vector marginals need a TransportGraph with k = shape[2]")
+        validate_norm(cfg.norm_u, "vector", "u")
+        validate_norm(cfg.norm_w, "vector", "w")
+        eng = build_engine("vector", n, cfg, graph=channels, precision=precision, device=device)
+        a, b = lambda0.to(torch.float64).contiguous(), lambda1.to(torch.float64).contiguous()
+    elif nd == 4:
+        if not isinstance(channels, LindbladSet) or channels.k != lambda0.shape[2]:
+            raise ValidationError("matrix marginals need a LindbladSet with k = shape[2]")
+        validate_norm(cfg.norm_u, "matrix", "u")
+        validate_norm(cfg.norm_w, "matrix", "w")
+        a = lambda0.to(torch.complex128).contiguous()
+        b = lambda1.to(torch.complex128).contiguous()
+        use_real = (NormFamily.L1NUC not in (cfg.norm_u, cfg.norm_w)
+                    and not bool(torch.any(a.imag != b.imag))
+                    and not np.any(np.asarray(channels.matrices).imag))
+        eng = build_engine("matrix", n, cfg, lindblad=channels, precision=precision,
+                           device=device, complex_path=not use_real)
+    else:
+        raise ValidationError(f"unsupported marginal rank {nd}")
+    try:
+        m0, m1 = eng.set_marginals_device(a, b)
+        _mass_check(m0, m1)
+        history, it, conv, wall = eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters,
+                                          cfg.check_every)
+        last = history[-1]
+        report = SolveReport(conv, it, last.primal, history, wall)
+        ux, uy, w, phi = eng.get_state_device()
+        if eng.kind == "scalar":
+            wobj = None
+        elif eng.kind == "vector":
+            wobj = _trusted(GraphFlux, values=w)
+        else:
+            wobj = _trusted(QuantumFlux, values=w)
+        state = SolverState(u=_trusted(FluxField, ux=ux, uy=uy), w=wobj, phi=phi, iteration=it,
+                            residual=last.residual, primal_value=last.primal,
+                            dual_value=last.dual, gap_ratio=last.gap_ratio,
+                            feas_residual=last.feas_residual)
+        return report, state  # close() drains the engine stream before freeing
+    finally:
+        eng.close()
 
 
 # ---------------------------------------------------------------------------

@@ -3,6 +3,9 @@ package's public API (the CUDA path)."""
 
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 
 import paper_1712_10279_b200 as pk
@@ -36,13 +39,26 @@ def solve_case(meta, l0, l1, lindblad=None, precision="f64", **over):
                            cfg=cfg, precision=precision)
 
 
+def _log_err(err):
+    """With OTFX_PARITY_LOG=<file>, record the worst relative error each test
+    measured (the parity table in profiles/ is built from this log)."""
+    path = os.environ.get("OTFX_PARITY_LOG")
+    if path:
+        test = os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0]
+        with open(path, "a") as f:
+            f.write(json.dumps({"test": test, "rel_err": err}) + "\n")
+
+
 def rel_err(a, b):
     a = np.asarray(a)
     b = np.asarray(b)
     scale = float(np.max(np.abs(b))) if b.size else 0.0
     if scale == 0.0:
-        return float(np.max(np.abs(a))) if a.size else 0.0
-    return float(np.max(np.abs(a - b))) / scale
+        err = float(np.max(np.abs(a))) if a.size else 0.0
+    else:
+        err = float(np.max(np.abs(a - b))) / scale
+    _log_err(err)
+    return err
 
 
 def hist_array(report):

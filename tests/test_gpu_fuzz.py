@@ -89,7 +89,7 @@ def _run_case(seed):
         eng = pdhg.OracleEngine("matrix", diff.astype(dt), n, tau, norm_u=nu, norm_w=nw,
                                 alpha=alpha, eps=eps, chan=chan, lam_chan=pk.lambda_max_L(lind),
                                 dtype=dt)
-        tol = 1e-9
+        tol = 1e-10
     _, _, hist = pdhg.oracle_run(eng, 1e-300, 1e-300, iters, ce)
     assert rep.iterations == iters
     g.hist_close(g.hist_array(rep), np.array(hist), tol)

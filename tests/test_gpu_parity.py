@@ -69,12 +69,12 @@ def test_golden_summary_fp64(name):
     rep, st = g.solve_case(meta, l0, l1, mats)
     assert rep.iterations == meta["iterations"]
     assert rep.converged == meta["converged"]
-    g.hist_close(g.hist_array(rep), arrs["history"], 1e-9)
+    g.hist_close(g.hist_array(rep), arrs["history"], 1e-10)
     norms = meta["norms"]
-    np.testing.assert_allclose(np.linalg.norm(st.phi), norms["phi"], rtol=1e-9)
-    np.testing.assert_allclose(np.linalg.norm(st.u.ux), norms["ux"], rtol=1e-9)
+    np.testing.assert_allclose(np.linalg.norm(st.phi), norms["phi"], rtol=1e-10)
+    np.testing.assert_allclose(np.linalg.norm(st.u.ux), norms["ux"], rtol=1e-10)
     if norms["w"] > 0:
-        np.testing.assert_allclose(np.linalg.norm(st.w.values), norms["w"], rtol=1e-9)
+        np.testing.assert_allclose(np.linalg.norm(st.w.values), norms["w"], rtol=1e-10)
 
 
 def test_converged_values_match_reference_acceptance():

@@ -23,7 +23,12 @@ def _rel(a, b):
     return float(np.max(np.abs(a - b))) / den if a.size else 0.0
 
 
-@pytest.mark.parametrize("name", gu.full_cases())
+# the BASELINE-size matrix fixtures take minutes through the NumPy oracle; the
+# GPU tests compare the CUDA path with them directly
+SLOW_FULL = {"B_matr256", "B_matc128"}
+
+
+@pytest.mark.parametrize("name", [c for c in gu.full_cases() if c not in SLOW_FULL])
 def test_oracle_matches_reference(name):
     meta, arrs = gu.load(name)
     eng = gu.oracle_engine(meta, arrs)
@@ -72,3 +77,16 @@ def test_generators_match_reference_bytes():
         for arr, key in ((a, "l0"), (b, "l1")):
             h = hashlib.sha256(np.ascontiguousarray(arr).tobytes()).hexdigest()
             assert h == idx[name]["sha256"][key], (name, key)
+
+
+def test_blas_rounding_model_of_graph_operators():
+    """The CUDA graph operators reproduce NumPy/OpenBLAS's fused multiply-add
+    order for S/graph.py:105-123 (tools/blas_order.py); pin the model on this
+    host's BLAS."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    import blas_order
+
+    assert blas_order.main(samples=40) == 0

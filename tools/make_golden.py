@@ -55,9 +55,9 @@ def cases():
     rng = np.random.default_rng(12345)
     out = []
 
-    def add(name, kind, l0, l1, chan, cfg, full=True, note=""):
+    def add(name, kind, l0, l1, chan, cfg, full=True, note="", marginals=True):
         out.append(dict(name=name, kind=kind, l0=l0, l1=l1, chan=chan, cfg=cfg,
-                        full=full, note=note))
+                        full=full, note=note, marginals=marginals))
 
     tri = of.triangle_graph()
     l0, l1 = of.rgb_disk_pair(of.GridSpec(64))
@@ -133,6 +133,21 @@ def cases():
     add("S_matc128", "matrix", C0, C1, lindblad_k2(),
         dict(tau=30.0, norm_u="l1nuc", norm_w="l1nuc", alpha=1.0, max_iters=300, check_every=100),
         full=False, note="C3: 2x2 complex 128^2 l1nuc, 300 iterations")
+    # -- full-state cases at the BASELINE sizes (the marginals are not stored:
+    # the tests regenerate them with paper_1712_10279_b200.synthetic and check
+    # the sha256 digests recorded here against the reference's bytes) -------
+    add("B_vec256", "vector", g0, g1, tri,
+        dict(tau=6.0, norm_u="l12", norm_w="l1", alpha=1.0, max_iters=400, check_every=100),
+        marginals=False, note="BASELINE C2 grid: full state after 400 iterations")
+    add("B_vec256_a03", "vector", g0, g1, tri,
+        dict(tau=6.0, norm_u="l12", norm_w="l1", alpha=0.3, max_iters=400, check_every=100),
+        marginals=False, note="BASELINE C2 grid at alpha=0.3 (w != 0), 400 iterations")
+    add("B_matr256", "matrix", M0, M1, L3,
+        dict(tau=30.0, norm_u="l2", norm_w="l1", alpha=1.0, max_iters=500, check_every=100),
+        marginals=False, note="BASELINE C4: full state after 500 iterations")
+    add("B_matc128", "matrix", C0, C1, lindblad_k2(),
+        dict(tau=30.0, norm_u="l1nuc", norm_w="l1nuc", alpha=1.0, max_iters=300, check_every=100),
+        marginals=False, note="BASELINE C3: full state after 300 iterations")
     r0, r1 = of.rgb_disk_pair(of.GridSpec(32))
     add("S_vec32_conv", "vector", r0, r1, tri,
         dict(tau=6.0, norm_u="l12", norm_w="l1", alpha=1.0), full=False,
@@ -178,8 +193,9 @@ def main(names=None):
                      phi=float(np.linalg.norm(st.phi)),
                      w=0.0 if wv is None else float(np.linalg.norm(wv)))
         if c["full"]:
-            arrs.update(l0=c["l0"].values, l1=c["l1"].values, ux=st.u.ux, uy=st.u.uy,
-                        phi=st.phi)
+            arrs.update(ux=st.u.ux, uy=st.u.uy, phi=st.phi)
+            if c["marginals"]:
+                arrs.update(l0=c["l0"].values, l1=c["l1"].values)
             if wv is not None:
                 arrs["w"] = wv
         chan = None
@@ -192,7 +208,8 @@ def main(names=None):
             arrs["lindblad"] = m
         np.savez_compressed(OUT / f"{c['name']}.npz", **arrs)
         index[c["name"]] = dict(kind=c["kind"], cfg=cfg, graph=chan, full=c["full"],
-                                note=c["note"], iterations=rep.iterations,
+                                note=c["note"], marginals=c["marginals"],
+                                iterations=rep.iterations,
                                 converged=bool(rep.converged),
                                 transport_value=rep.transport_value, norms=norms,
                                 phi_dtype=str(st.phi.dtype), seconds=round(dt, 2),
