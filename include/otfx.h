@@ -195,9 +195,13 @@ int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_poi
                     int64_t capacity, int64_t* n_history, int64_t* iterations, int* converged,
                     double* wall_seconds);
 /* the same run loop over the row slabs of one grid held by `count` engines on
- * one device and one stream (in row order, diff norms already combined),
- * stepped in lockstep with local halo copies: the single-GPU stand-in for the
- * NCCL-connected ranks (same check cadence, fused checks and stopping rule) */
+ * one device and one stream (in row order), stepped in lockstep: the
+ * single-GPU stand-in for the NCCL-connected ranks (same check cadence, fused
+ * checks and stopping rule, and the same halo pack -> transport -> unpack as
+ * exchange over NCCL, the transport being device copies between the slabs'
+ * send / receive buffers).  The whole-grid ||diff|| is combined from the
+ * slabs' own-row norms (overrides set with otfx_engine_diff_norm are not
+ * used here). */
 int otfx_engines_run_local(otfx_engine* const* engines, int count, const otfx_run_config* cfg,
                            otfx_history_point* history, int64_t capacity, int64_t* n_history,
                            int64_t* iterations, int* converged);

@@ -293,7 +293,8 @@ struct otfx_engine {
   double* h_raw = nullptr;         // pinned
   int ex = 1, ey = 1;
   bool residual_valid = false;
-  double diff_norm = 0.0;
+  double diff_norm = 0.0;       // ||diff|| of the whole grid (allreduced across ranks)
+  double diff_norm_own = 0.0;   // ||diff|| of this slab's own rows
   // staging for host <-> device conversions
   double* d_stage = nullptr;
   size_t stage_bytes = 0;
@@ -554,62 +555,123 @@ static void launch_evaluate(otfx_engine* e) {
   else launch_evaluate<float>(e);
 }
 
-// halo rows: top ghost (local 0) <- previous slab's last row (phi + u);
-// bottom ghost (local rows+1) <- next slab's first row (phi)
-static void copy_rows(otfx_engine* dst, void* dbase, int drow, otfx_engine* src, void* sbase,
-                      int srow, int nplanes, cudaStream_t s) {
-  // plane strides differ between slabs of different heights
-  const size_t w = size_t(dst->d.n) * dst->elem;
-  const size_t dpb = size_t(dst->plane) * dst->elem, spb = size_t(src->plane) * src->elem;
-  CK(cudaMemcpy2DAsync(static_cast<char*>(dbase) + size_t(drow) * dst->pitch * dst->elem, dpb,
-                       static_cast<char*>(sbase) + size_t(srow) * src->pitch * src->elem, spb, w,
-                       nplanes, cudaMemcpyDeviceToDevice, s));
+// ---- halo exchange: pack -> transport -> unpack ----------------------------
+// One layout for every transport.  e->d_halo holds four contiguous buffers of
+// n-element rows ([row][n], the planes of one grid row stacked):
+//   send_top  NP rows   phi of the first owned row          -> previous slab
+//   send_bot  3NP rows  phi, u (2NP planes) of the last row  -> next slab
+//   recv_top  3NP rows  <- previous slab's send_bot  (unpacked into local row 0)
+//   recv_bot  NP rows   <- next slab's send_top      (unpacked into row rows+1)
+// Rows [0, rows+1] of a slab: 0 and rows+1 are the ghost rows the stencils
+// read (S/spatial.py:30-37 needs ubar_x(i-1); S/spatial.py:80-86 phi(i+1)).
+// pack/unpack are one kernel each; the transport is NCCL send/recv between
+// ranks (exchange_nccl) or device copies between the slabs of one process
+// (exchange_local_impl), so the single-GPU slab groups run the exact buffer
+// layout and kernels the NCCL ranks run.
+struct RowSeg {
+  const char* src;
+  char* dst;
+  long long src_stride, dst_stride;  // bytes between consecutive planes / rows
+  int planes;
+};
+struct RowSegs {
+  RowSeg s[3];
+  int nseg = 0;
+  int planes = 0;  // total
+};
+
+template <typename W>
+__global__ void row_copy_kernel(const __grid_constant__ RowSegs m, int n) {
+  int p = blockIdx.y, q = 0;
+  while (q + 1 < m.nseg && p >= m.s[q].planes) p -= m.s[q++].planes;
+  const W* src = reinterpret_cast<const W*>(m.s[q].src + p * m.s[q].src_stride);
+  W* dst = reinterpret_cast<W*>(m.s[q].dst + p * m.s[q].dst_stride);
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    dst[j] = src[j];
+}
+
+struct HaloBufs {
+  char *send_top, *send_bot, *recv_top, *recv_bot;
+};
+
+static HaloBufs halo_bufs(const otfx_engine* e) {
+  const size_t wb = size_t(e->d.n) * e->elem;
+  char* b = static_cast<char*>(e->d_halo);
+  HaloBufs h;
+  h.send_top = b;
+  h.send_bot = h.send_top + e->NP * wb;
+  h.recv_top = h.send_bot + 3 * e->NP * wb;
+  h.recv_bot = h.recv_top + 3 * e->NP * wb;
+  return h;
+}
+
+static void add_seg(RowSegs& m, const void* src, long long ss, void* dst, long long ds, int planes) {
+  m.s[m.nseg++] = {static_cast<const char*>(src), static_cast<char*>(dst), ss, ds, planes};
+  m.planes += planes;
+}
+
+static void launch_row_copy(const otfx_engine* e, const RowSegs& m, cudaStream_t st) {
+  if (!m.planes) return;
+  const int n = e->d.n;
+  dim3 grid(std::min((n + 255) / 256, 16), m.planes);
+  if (e->elem == 8) row_copy_kernel<double><<<grid, 256, 0, st>>>(m, n);
+  else row_copy_kernel<float><<<grid, 256, 0, st>>>(m, n);
+  CK(cudaGetLastError());
+}
+
+static char* row_of(const otfx_engine* e, void* base, int lrow) {
+  return static_cast<char*>(base) + size_t(lrow) * e->pitch * e->elem;
+}
+
+// boundary rows of the current iterate -> send buffers
+static void halo_pack(const otfx_engine* e, bool has_prev, bool has_next, cudaStream_t st) {
+  const HaloBufs h = halo_bufs(e);
+  const long long pb = (long long)e->plane * e->elem, wb = (long long)e->d.n * e->elem;
+  const int c = e->cur, NP = e->NP;
+  RowSegs m;
+  if (has_prev) add_seg(m, row_of(e, e->phi[c], 1), pb, h.send_top, wb, NP);
+  if (has_next) {
+    add_seg(m, row_of(e, e->phi[c], e->rows), pb, h.send_bot, wb, NP);
+    add_seg(m, row_of(e, e->u[c], e->rows), pb, h.send_bot + NP * wb, wb, 2 * NP);
+  }
+  launch_row_copy(e, m, st);
+}
+
+// receive buffers -> ghost rows of the current iterate
+static void halo_unpack(const otfx_engine* e, bool has_prev, bool has_next, cudaStream_t st) {
+  const HaloBufs h = halo_bufs(e);
+  const long long pb = (long long)e->plane * e->elem, wb = (long long)e->d.n * e->elem;
+  const int c = e->cur, NP = e->NP;
+  RowSegs m;
+  if (has_prev) {
+    add_seg(m, h.recv_top, wb, row_of(e, e->phi[c], 0), pb, NP);
+    add_seg(m, h.recv_top + NP * wb, wb, row_of(e, e->u[c], 0), pb, 2 * NP);
+  }
+  if (has_next) add_seg(m, h.recv_bot, wb, row_of(e, e->phi[c], e->rows + 1), pb, NP);
+  launch_row_copy(e, m, st);
 }
 
 static void exchange_nccl(otfx_engine* e, cudaStream_t st) {
   if (!e->comm || e->nranks == 1) return;
   NcclApi& N = nccl();
-  const int c = e->cur;
-  const size_t w = size_t(e->d.n);
-  const size_t pb = size_t(e->plane) * e->elem;
-  const size_t wb = w * e->elem;
-  const int NP = e->NP;
-  char* buf = static_cast<char*>(e->d_halo);
-  char* send_top = buf;                       // NP rows: phi(first row) -> rank-1
-  char* send_bot = send_top + NP * wb;        // 3NP rows: phi, u (last row) -> rank+1
-  char* recv_top = send_bot + 3 * NP * wb;    // 3NP rows from rank-1
-  char* recv_bot = recv_top + 3 * NP * wb;    // NP rows from rank+1
-  auto rowp = [&](void* base, int lrow) {
-    return static_cast<char*>(base) + size_t(lrow) * e->pitch * e->elem;
-  };
   const bool has_prev = e->rank > 0, has_next = e->rank + 1 < e->nranks;
-  if (has_prev) CK(cudaMemcpy2DAsync(send_top, wb, rowp(e->phi[c], 1), pb, wb, NP, cudaMemcpyDeviceToDevice, st));
-  if (has_next) {
-    CK(cudaMemcpy2DAsync(send_bot, wb, rowp(e->phi[c], e->rows), pb, wb, NP, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpy2DAsync(send_bot + NP * wb, wb, rowp(e->u[c], e->rows), pb, wb, 2 * NP,
-                         cudaMemcpyDeviceToDevice, st));
-  }
+  const size_t w = size_t(e->d.n);
+  const int NP = e->NP;
+  const HaloBufs h = halo_bufs(e);
+  halo_pack(e, has_prev, has_next, st);
   const ncclDataType_t dt = e->elem == 8 ? ncclFloat64 : ncclFloat32;
   NK(N.GroupStart());
   if (has_prev) {
-    NK(N.Send(send_top, NP * w, dt, e->rank - 1, e->comm, st));
-    NK(N.Recv(recv_top, 3 * NP * w, dt, e->rank - 1, e->comm, st));
+    NK(N.Send(h.send_top, NP * w, dt, e->rank - 1, e->comm, st));
+    NK(N.Recv(h.recv_top, 3 * NP * w, dt, e->rank - 1, e->comm, st));
   }
   if (has_next) {
-    NK(N.Send(send_bot, 3 * NP * w, dt, e->rank + 1, e->comm, st));
-    NK(N.Recv(recv_bot, NP * w, dt, e->rank + 1, e->comm, st));
+    NK(N.Send(h.send_bot, 3 * NP * w, dt, e->rank + 1, e->comm, st));
+    NK(N.Recv(h.recv_bot, NP * w, dt, e->rank + 1, e->comm, st));
   }
   NK(N.GroupEnd());
-  if (has_prev) {
-    CK(cudaMemcpy2DAsync(rowp(e->phi[c], 0), pb, recv_top, wb, wb, NP, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpy2DAsync(rowp(e->u[c], 0), pb, recv_top + NP * wb, wb, wb, 2 * NP,
-                         cudaMemcpyDeviceToDevice, st));
-  }
-  if (has_next)
-    CK(cudaMemcpy2DAsync(rowp(e->phi[c], e->rows + 1), pb, recv_bot, wb, wb, NP,
-                         cudaMemcpyDeviceToDevice, st));
+  halo_unpack(e, has_prev, has_next, st);
 }
-
 
 static void exchange_nccl(otfx_engine* e) { exchange_nccl(e, e->stream); }
 
@@ -838,7 +900,11 @@ static void launch_cluster(otfx_engine* e, const otfx_run_config* cfg, int64_t p
 }
 
 // S/solver.py:242-291 scalar algebra, same operation order
+static void finalize(const otfx_engine* e, const double* raw, double out[5], double diff_norm);
 static void finalize(const otfx_engine* e, const double* raw, double out[5]) {
+  finalize(e, raw, out, e->diff_norm);
+}
+static void finalize(const otfx_engine* e, const double* raw, double out[5], double diff_norm) {
   const bool has_w = e->has_w;
   const double alpha = e->d.alpha, eps = e->d.eps_reg;
   double p = raw[R_PU];
@@ -860,7 +926,7 @@ static void finalize(const otfx_engine* e, const double* raw, double out[5]) {
   }
   const double gap = (p - dual) / std::max(p, 1e-30);
   const double tiny = 2.2250738585072014e-308;
-  const double feas = std::sqrt(raw[R_SCON]) / std::max(e->diff_norm, tiny);
+  const double feas = std::sqrt(raw[R_SCON]) / std::max(diff_norm, tiny);
   double r = raw[R_SDU] / e->d.mu + raw[R_SDPHI] / e->d.tau;
   if (has_w) r += raw[R_SDW] / e->d.nu;
   r = r - 2.0 * raw[R_SCROSS];
@@ -1601,6 +1667,9 @@ struct SlabGroup {
   otfx_engine* lead() const { return es[0]; }
 };
 
+// the slabs of one grid in one process: same pack / unpack as exchange_nccl,
+// the transport is a device copy of each send buffer into the neighbour's
+// receive buffer (what ncclSend/ncclRecv move between ranks)
 static void exchange_local_impl(otfx_engine* const* es, int count, cudaStream_t st) {
   for (int s = 0; s + 1 < count; ++s) {
     otfx_engine* a = es[s];
@@ -1610,13 +1679,16 @@ static void exchange_local_impl(otfx_engine* const* es, int count, cudaStream_t 
                 a->NP == b->NP && a->pitch == b->pitch,
             OTFX_EINVAL, "engines are not adjacent slabs of one grid");
     require(a->cur == b->cur, OTFX_EINVAL, "engines are at different iterations");
-    const int c = a->cur;
-    // a's bottom ghost <- b's first row (phi)
-    copy_rows(a, a->phi[c], a->rows + 1, b, b->phi[c], 1, a->NP, st);
-    // b's top ghost <- a's last row (phi, u)
-    copy_rows(b, b->phi[c], 0, a, a->phi[c], a->rows, a->NP, st);
-    copy_rows(b, b->u[c], 0, a, a->u[c], a->rows, 2 * a->NP, st);
   }
+  for (int s = 0; s < count; ++s) halo_pack(es[s], s > 0, s + 1 < count, st);
+  for (int s = 0; s + 1 < count; ++s) {
+    const HaloBufs ha = halo_bufs(es[s]), hb = halo_bufs(es[s + 1]);
+    const size_t wb = size_t(es[s]->d.n) * es[s]->elem;
+    const int NP = es[s]->NP;
+    CK(cudaMemcpyAsync(hb.recv_top, ha.send_bot, 3 * NP * wb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(ha.recv_bot, hb.send_top, NP * wb, cudaMemcpyDeviceToDevice, st));
+  }
+  for (int s = 0; s < count; ++s) halo_unpack(es[s], s > 0, s + 1 < count, st);
 }
 
 // one iteration of every slab, then the halo exchange (overlapped with the
@@ -1662,6 +1734,15 @@ static void group_raw(const SlabGroup& g, bool fused, bool with_res, double raw[
 static void run_loop(const SlabGroup& g, const otfx_run_config* cfg, otfx_history_point* hist,
                      int64_t capacity, int64_t* n_history, int64_t* iterations, int* converged) {
   otfx_engine* e = g.lead();
+  // ||diff|| of the whole grid: the engine's (allreduced under NCCL), or for a
+  // local slab group the root of the slabs' summed squares, combined here
+  // from every slab's own-row norm (S/solver.py:185)
+  double dn = e->diff_norm;
+  if (g.local()) {
+    double s2 = 0.0;
+    for (int q = 0; q < g.count; ++q) s2 += g.es[q]->diff_norm_own * g.es[q]->diff_norm_own;
+    dn = std::sqrt(s2);
+  }
   int64_t nh = 0;
   auto push = [&](int64_t it, const double* r, double rk) {
     require(nh < capacity, OTFX_EINVAL, "history buffer too small");
@@ -1669,7 +1750,7 @@ static void run_loop(const SlabGroup& g, const otfx_run_config* cfg, otfx_histor
   };
   double r[5], raw[OTFX_NRAW];
   group_raw(g, false, false, raw);
-  finalize(e, raw, r);
+  finalize(e, raw, r, dn);
   push(0, r, std::nan(""));
   bool conv = r[2] <= cfg->tol_gap && r[3] <= cfg->tol_feas;
   int64_t it = 0;
@@ -1688,7 +1769,7 @@ static void run_loop(const SlabGroup& g, const otfx_run_config* cfg, otfx_histor
     group_sweep(g, 1);
     if (fuse) group_sweep(g, 2);
     group_raw(g, fuse, true, raw);
-    finalize(e, raw, r);
+    finalize(e, raw, r, dn);
     it = next;
     push(it, r, r[4]);
     conv = r[2] <= cfg->tol_gap && r[3] <= cfg->tol_feas;
@@ -1825,6 +1906,7 @@ static PackMap marginals_map(const otfx_engine* e) {
 }
 
 static void take_marginal_sums(otfx_engine* e, double sums[3], double masses[2]) {
+  e->diff_norm_own = std::sqrt(sums[2]);
   allreduce_host(e, sums, 3);
   e->diff_norm = std::sqrt(sums[2]);
   if (masses) {
@@ -1903,6 +1985,7 @@ int otfx_engine_set_diff(otfx_engine* e, const double* diff) {
   PackMap m = potential_pack(e, e->d.kind == OTFX_KIND_MATRIX_COMPLEX);
   double sums[3];
   host_to_planes(e, diff, nullptr, m, e->diff, sums);
+  e->diff_norm_own = std::sqrt(sums[2]);
   allreduce_host(e, sums, 3);
   e->diff_norm = std::sqrt(sums[2]);
   API_END

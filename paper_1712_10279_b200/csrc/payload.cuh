@@ -34,6 +34,37 @@ __device__ __forceinline__ T soft_factor(T r, T thr) {
 template <typename T>
 __device__ __forceinline__ T sq(T x) { return x * x; }
 
+// Sum of squares in NumPy's einsum order.  The reference's block norms are
+// np.einsum("...i,...i->...", x, x) over the contiguous payload
+// (S/shrink.py:88-104), whose inner loop (sum_of_products_contig_contig_
+// outstride0_two, baseline SSE2 build: two double lanes, multiply then add)
+// runs blocks of 8 elements as  lane += x[6+l]^2, x[4+l]^2, x[2+l]^2, x[l]^2,
+// then the rest two at a time, and returns lane0 + lane1.  `len` (<= N) is
+// the runtime block length; entries past it are not touched.
+// tools/einsum_order.py checks this model against NumPy.
+template <int N, typename T>
+__device__ __forceinline__ T np_sumsq(const T* x, int len) {
+  T a0 = T(0), a1 = T(0);
+  int done = 0;
+#pragma unroll
+  for (int b = 0; b + 8 <= N; b += 8) {
+    if (b + 8 <= len) {
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        a0 = x[b + 2 * q] * x[b + 2 * q] + a0;
+        a1 = x[b + 2 * q + 1] * x[b + 2 * q + 1] + a1;
+      }
+      done = b + 8;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; i += 2) {
+    if (i >= done && i < len) a0 = x[i] * x[i] + a0;
+    if (i + 1 < N && i + 1 >= done && i + 1 < len) a1 = x[i + 1] * x[i + 1] + a1;
+  }
+  return a0 + a1;
+}
+
 // ===========================================================================
 // vector / scalar payloads
 // ===========================================================================
@@ -57,11 +88,8 @@ struct VecPolicy {
   __device__ static void prox_u(T (&x)[2][NP], const PA& A) {
     const T thr = A.mu;
     if (A.norm_u == NORM_L2) {
-      T s = T(0);
-#pragma unroll
-      for (int d = 0; d < 2; ++d)
-#pragma unroll
-        for (int c = 0; c < K; ++c) s = s + x[d][c] * x[d][c];
+      // the (2, k) payload block in C order (S/shrink.py:107-108)
+      const T s = np_sumsq<2 * K>(&x[0][0], 2 * K);
       const T f = soft_factor(sqrt(s), thr);
 #pragma unroll
       for (int d = 0; d < 2; ++d)
@@ -128,9 +156,7 @@ struct VecPolicy {
   __device__ static void prox_w(T (&x)[NWA], const PA& A) {
     const T thr = A.thr_w;
     if (A.norm_w == NORM_L2) {
-      T s = T(0);
-#pragma unroll
-      for (int e = 0; e < NWA; ++e) s = s + x[e] * x[e];
+      const T s = np_sumsq<NWA>(x, A.ell);
       const T f = soft_factor(sqrt(s), thr);
 #pragma unroll
       for (int e = 0; e < NWA; ++e) x[e] = x[e] * f;

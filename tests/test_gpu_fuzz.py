@@ -97,6 +97,12 @@ def _run_case(seed):
     assert g.rel_err(st.u.ux, eng.u[:, :, 0]) <= tol
     if st.w is not None:
         assert g.rel_err(st.w.values, eng.w) <= tol
+    if kind in ("scalar", "vector"):
+        # same rounding sequence as the reference: equal bits
+        assert np.array_equal(st.phi, eng.phi)
+        assert np.array_equal(st.u.ux, eng.u[:, :, 0]) and np.array_equal(st.u.uy, eng.u[:, :, 1])
+        if st.w is not None:
+            assert np.array_equal(st.w.values, eng.w)
 
 
 @pytest.mark.parametrize("path", ["default", "register", "tma"])

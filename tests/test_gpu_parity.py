@@ -39,6 +39,14 @@ def test_golden_full_fp64(name, sweep, monkeypatch):
     if "w" in arrs:
         assert st.w.values.shape == arrs["w"].shape
         assert g.rel_err(st.w.values, arrs["w"]) <= F64_RTOL
+    if meta["kind"] in ("scalar", "vector"):
+        # these paths follow the reference's rounding sequence exactly
+        # (IEEE div/sqrt, no contraction, the BLAS order of the graph
+        # operators): the reference's own iterates, bit for bit
+        assert np.array_equal(st.u.ux, arrs["ux"]) and np.array_equal(st.u.uy, arrs["uy"])
+        assert np.array_equal(st.phi, arrs["phi"])
+        if "w" in arrs:
+            assert np.array_equal(st.w.values, arrs["w"])
 
 
 @pytest.mark.parametrize("name", gu.full_cases())

@@ -167,14 +167,18 @@ def test_bench_reference_arm_contract():
     import sys
 
     cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
-           "--warmup", "1", "--ref-n", "48"]
+           "--warmup", "1", "--ref-n", "48", "--n", "48"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, check=True)
     line = json.loads(out.stdout.strip().splitlines()[-1])
     for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
                 "higher_is_better", "cpu_baseline", "e2e", "config"):
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
-    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
+    # the unmodified reference from baseline/_ref when installed,
+    # else the NumPy port
+    installed = (ROOT / "baseline" / "_ref" / "otflux").is_dir()
+    assert line["cpu_baseline"]["kind"] == ("reference" if installed else "port")
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["config"]["sample_n"] == 48
     env = dict(os.environ, RANK="1", WORLD_SIZE="2")
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env,
                          check=True)

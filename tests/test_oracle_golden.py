@@ -90,3 +90,15 @@ def test_blas_rounding_model_of_graph_operators():
     import blas_order
 
     assert blas_order.main(samples=40) == 0
+
+
+def test_einsum_summation_model_of_block_norms():
+    """The CUDA block norms reproduce np.einsum's summation order for
+    S/shrink.py:88-104 (tools/einsum_order.py); pin the model here."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    import einsum_order
+
+    assert einsum_order.main(cells=100) == 0

@@ -23,9 +23,6 @@ engs = [build_engine("vector", n, cfg, graph=pk.triangle_graph(), rows=(bounds[r
                      stream=s.cuda_stream) for r in range(P)]
 for r, e in enumerate(engs):
     e.set_marginals(l0[bounds[r]:bounds[r + 1]], l1[bounds[r]:bounds[r + 1]])
-dn = float(np.sqrt(sum(e.diff_norm ** 2 for e in engs)))
-for e in engs:
-    e.diff_norm = dn
 run_local(engs, 1e-300, 1e-300, 100, 100)
 torch.cuda.synchronize()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
