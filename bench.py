@@ -498,7 +498,12 @@ def matrix_roofline(args, device):
     cases = [("C4 family: 3x3 real-symmetric DTI, l2/l1, 2 Lindblad", synthetic.matrix_blob_fixtures,
               pk.default_lindblad3(), ("l2", "l1"), False, 7 * 6 + 2 * 2 * 3),
              ("C3 family: 2x2 complex Hermitian, l1nuc/l1nuc, 2 Lindblad", synthetic.blob_pair_k2,
-              pk.lindblad_pair_k2(), ("l1nuc", "l1nuc"), True, (7 + 2 * 2) * 4)]
+              pk.lindblad_pair_k2(), ("l1nuc", "l1nuc"), True, (7 + 2 * 2) * 4),
+             # the heaviest payloads (3x3 complex Hermitian: 2 + 2 eigensolves per cell)
+             ("3x3 complex Hermitian, l1nuc/l1nuc, 2 Lindblad", synthetic.matrix_blob_fixtures,
+              pk.default_lindblad3(), ("l1nuc", "l1nuc"), True, (7 + 2 * 2) * 9),
+             ("3x3 complex Hermitian, l2/l1, 2 Lindblad", synthetic.matrix_blob_fixtures,
+              pk.default_lindblad3(), ("l2", "l1"), True, (7 + 2 * 2) * 9)]
     for name, gen, lind, norms, cplx, words in cases:
         l0, l1 = gen(n)[:2]
         cfg = pk.SolverConfig(tau=30.0, norm_u=norms[0], norm_w=norms[1])

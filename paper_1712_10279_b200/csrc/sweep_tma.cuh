@@ -105,6 +105,54 @@ struct StageShape {
   static constexpr int BYTES = OFF_P + R128(P::NP * ROW);
 };
 
+// The producer warp's loop (one elected lane): stage q of the ring gets
+// global row qbase + q -- the halo row (u, phi), the R owned rows (u, w, diff,
+// phi), the phi-only tail row -- each a set of 3-D TMA boxes completing on
+// full[slot]; a slot is reused once every consumer warp has arrived on
+// empty[slot].
+template <class SS, class P, typename T>
+__device__ __forceinline__ void tma_produce(const SweepArgs<T>& A, const StageLayout& L,
+                                            const TmaSet& M, uint64_t* full, uint64_t* empty,
+                                            unsigned char* stages, int c0, int gr0, int gr1,
+                                            int qbase, int qmax) {
+  const int S = L.S;
+  const int n = A.n;
+
+  const int cx = c0 - SS::H;
+  int slot = 0, use = 0;
+  for (int q = 0; q <= qmax; ++q) {
+    if (q >= S) mbar_wait(&empty[slot], (use - 1) & 1);
+    uint64_t* bar = &full[slot];
+    const int r = qbase + q;
+    const int lrow = r - A.row_begin + 1;
+    unsigned char* st = stages + slot * SS::BYTES;
+    if (q == 0 || q == qmax) {
+      const bool load = (q == 0) ? (gr0 > 0) : (r < n);
+      if (!load) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+      } else {
+        if (q == 0) {
+          mbar_expect_tx(bar, L.bytes_flux);
+          tma_load_3d(st, &M.u, bar, cx, lrow, 0);
+        } else {
+          mbar_expect_tx(bar, L.bytes_phi);
+        }
+        tma_load_3d(st + SS::OFF_P, &M.phi, bar, cx, lrow, 0);
+      }
+    } else {
+      mbar_expect_tx(bar, L.bytes_full);
+      tma_load_3d(st, &M.u, bar, cx, lrow, 0);
+      if (P::HAS_W) tma_load_3d(st + SS::OFF_W, &M.w, bar, cx, lrow, 0);
+      tma_load_3d(st + SS::OFF_D, &M.diff, bar, cx, lrow, 0);
+      tma_load_3d(st + SS::OFF_P, &M.phi, bar, cx, lrow, 0);
+    }
+    if (++slot == S) {
+      slot = 0;
+      ++use;
+    }
+  }
+}
+
 // FL bit 0 (CHECK): this sweep ends on a check iteration -- accumulate the
 //   R^k terms (S/solver.py:282-291) from the old and new values in registers;
 // FL bit 1 (DUAL): the INPUT iterate is a checked one -- accumulate its
@@ -169,42 +217,7 @@ __global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) :
   double acc[4] = {0, 0, 0, 0};
   double dsum[8] = {0, 0, 0, 0, 0, 0, 0, 0}, dmx[2] = {0.0, 0.0};
   if (producer) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      const int cx = c0 - SS::H;
-      int slot = 0, use = 0;
-      for (int q = 0; q <= qmax; ++q) {
-        if (q >= S) mbar_wait(&empty[slot], (use - 1) & 1);
-        uint64_t* bar = &full[slot];
-        const int r = qbase + q;
-        const int lrow = r - A.row_begin + 1;
-        unsigned char* st = stages + slot * SS::BYTES;
-        if (q == 0 || q == qmax) {
-          const bool load = (q == 0) ? (gr0 > 0) : (r < n);
-          if (!load) {
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-          } else {
-            if (q == 0) {
-              mbar_expect_tx(bar, L.bytes_flux);
-              tma_load_3d(st, &M.u, bar, cx, lrow, 0);
-            } else {
-              mbar_expect_tx(bar, L.bytes_phi);
-            }
-            tma_load_3d(st + SS::OFF_P, &M.phi, bar, cx, lrow, 0);
-          }
-        } else {
-          mbar_expect_tx(bar, L.bytes_full);
-          tma_load_3d(st, &M.u, bar, cx, lrow, 0);
-          if (P::HAS_W) tma_load_3d(st + SS::OFF_W, &M.w, bar, cx, lrow, 0);
-          tma_load_3d(st + SS::OFF_D, &M.diff, bar, cx, lrow, 0);
-          tma_load_3d(st + SS::OFF_P, &M.phi, bar, cx, lrow, 0);
-        }
-        if (++slot == S) {
-          slot = 0;
-          ++use;
-        }
-      }
-    }
+    if (lane == 0) tma_produce<SS, P, T>(A, L, M, full, empty, stages, c0, gr0, gr1, qbase, qmax);
   } else {
     // ------------------------------------------------------------ consumers
     HotArgs<P, T> H;
