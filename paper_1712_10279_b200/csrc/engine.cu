@@ -1055,15 +1055,18 @@ static PackMap flux_w_pack(const otfx_engine* e) {
     }
     return m;
   }
-  m.rec = 2 * ell * K * K;
+  // real path: w is a float64 (ell, K, K) record, as the reference's real
+  // engine holds it (S/solver.py:414-432); complex path: complex128
+  const int cs = e->d.kind == OTFX_KIND_MATRIX_REAL ? 1 : 2;
+  m.rec = cs * ell * K * K;
   const int NWS = e->NWS;
   for (int s = 0; s < ell; ++s) {
-    const int base = 2 * s * K * K;
+    const int base = cs * s * K * K;
     if (e->d.kind == OTFX_KIND_MATRIX_REAL) {
       for (int a = 0; a < K; ++a)
         for (int b = a + 1; b < K; ++b) {
           const int p = s * NWS + pair_index_rt(K, a, b);
-          m.src[p] = base + 2 * (a * K + b);
+          m.src[p] = base + (a * K + b);
           m.wt[p] = 2.0;
         }
     } else {
@@ -1096,13 +1099,14 @@ static UnpackMap flux_w_unpack(const otfx_engine* e) {
     for (int q = 0; q < ell; ++q) m.plane[q] = q;
     return m;
   }
-  m.rec = 2 * ell * K * K;
+  const int cs = e->d.kind == OTFX_KIND_MATRIX_REAL ? 1 : 2;
+  m.rec = cs * ell * K * K;
   const int NWS = e->NWS;
   for (int s = 0; s < ell; ++s) {
-    const int base = 2 * s * K * K;
+    const int base = cs * s * K * K;
     for (int a = 0; a < K; ++a)
       for (int b = 0; b < K; ++b) {
-        const int q = base + 2 * (a * K + b);
+        const int q = base + cs * (a * K + b);
         if (e->d.kind == OTFX_KIND_MATRIX_REAL) {
           if (a == b) continue;
           m.plane[q] = s * NWS + pair_index_rt(K, std::min(a, b), std::max(a, b));

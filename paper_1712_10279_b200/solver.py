@@ -238,6 +238,11 @@ class CudaEngine:
     def _pdtype(self):
         return np.complex128 if self.kind == "matrix_complex" else np.float64
 
+    def _wdtype(self):
+        """w is real for the vector and real-symmetric matrix paths (the
+        reference's real engine holds w as float64, S/solver.py:414-432)."""
+        return np.complex128 if self.kind == "matrix_complex" else np.float64
+
     def _wshape(self):
         if self.kind == "vector":
             return (self.ell,)
@@ -278,7 +283,7 @@ class CudaEngine:
         uy = np.ascontiguousarray(uy, dtype=pdt)
         phi = np.ascontiguousarray(phi, dtype=pdt)
         if w is not None:
-            w = np.ascontiguousarray(w, dtype=np.float64 if self.kind == "vector" else np.complex128)
+            w = np.ascontiguousarray(w, dtype=self._wdtype())
         _lib.check(self._lib.otfx_engine_set_state(self._h, _ptr(ux), _ptr(uy), _ptr(w), _ptr(phi)))
 
     def alloc_state(self, prefault=False):
@@ -292,8 +297,7 @@ class CudaEngine:
         phi = np.empty(shape, pdt)
         w = None
         if self.kind != "scalar":
-            w = np.empty((self.nrows, self.n) + self._wshape(),
-                         np.float64 if self.kind == "vector" else np.complex128)
+            w = np.empty((self.nrows, self.n) + self._wshape(), self._wdtype())
         if prefault:
             for a in (ux, uy, w, phi):
                 if a is not None:
@@ -305,7 +309,7 @@ class CudaEngine:
         per = int(np.prod(self._pshape(), dtype=np.int64)) * np.dtype(self._pdtype()).itemsize
         wb = 0
         if self.kind != "scalar":
-            wb = int(np.prod(self._wshape(), dtype=np.int64)) * (8 if self.kind == "vector" else 16)
+            wb = int(np.prod(self._wshape(), dtype=np.int64)) * np.dtype(self._wdtype()).itemsize
         return cells * (3 * per + wb)
 
     def prefault_async(self):
@@ -362,7 +366,7 @@ class CudaEngine:
 
     def set_state_device(self, ux, uy, w, phi, stream=None):
         pdt = self._pdtype()
-        wdt = np.float64 if self.kind == "vector" else np.complex128
+        wdt = self._wdtype()
         _lib.check(self._lib.otfx_engine_set_state_device(
             self._h, self._tensor_ptr(ux, pdt), self._tensor_ptr(uy, pdt),
             self._tensor_ptr(w, wdt), self._tensor_ptr(phi, pdt), self._torch_stream(stream)))
@@ -379,7 +383,7 @@ class CudaEngine:
         phi = torch.empty_like(ux)
         w = None
         if self.kind != "scalar":
-            wdt = torch.float64 if self.kind == "vector" else torch.complex128
+            wdt = torch.complex128 if self._wdtype() == np.complex128 else torch.float64
             w = torch.empty((self.nrows, self.n) + self._wshape(), dtype=wdt, device=dev)
         return ux, uy, w, phi
 
@@ -388,7 +392,7 @@ class CudaEngine:
         stream order (no host round trip)."""
         ux, uy, w, phi = out if out is not None else self.alloc_state_device()
         pdt = self._pdtype()
-        wdt = np.float64 if self.kind == "vector" else np.complex128
+        wdt = self._wdtype()
         _lib.check(self._lib.otfx_engine_get_state_device(
             self._h, self._tensor_ptr(ux, pdt), self._tensor_ptr(uy, pdt),
             self._tensor_ptr(w, wdt), self._tensor_ptr(phi, pdt), self._torch_stream(stream)))
@@ -780,7 +784,7 @@ def residual_Rk(state_prev: SolverState, state_next: SolverState, mu: float, nu:
                      device=device, **extra)
     try:
         pdt = eng._pdtype()
-        wdt = np.float64 if kind == "vector" else np.complex128
+        wdt = eng._wdtype()
         arrs = []
         for st in (state_prev, state_next):
             w = None if st.w is None else np.ascontiguousarray(st.w.values, dtype=wdt)

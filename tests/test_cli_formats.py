@@ -3,15 +3,24 @@ OMTF / graph / Lindblad files written by the reference are read identically
 and re-written byte for byte; argument and input errors map to the
 reference's exit codes without touching a GPU."""
 
+import contextlib
+import io
 import json
 from pathlib import Path
 
 import numpy as np
-from click.testing import CliRunner
 
 import paper_1712_10279_b200 as pk
 from paper_1712_10279_b200 import omtf
 from paper_1712_10279_b200.cli import main
+
+
+def _cli(args):
+    """Run the CLI in-process: (exit code, stdout + stderr)."""
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf), contextlib.redirect_stderr(buf):
+        code = main([str(a) for a in args])
+    return code, buf.getvalue()
 
 G = Path(__file__).resolve().parent / "golden" / "omtf"
 
@@ -39,23 +48,23 @@ def test_graph_and_lindblad_files(tmp_path):
 
 
 def test_cli_input_errors_exit_2(tmp_path):
-    r = CliRunner().invoke(main, ["solve", "vector", "--lambda0", str(tmp_path / "missing.omtf"),
+    code, output = _cli(["solve", "vector", "--lambda0", str(tmp_path / "missing.omtf"),
                                   "--lambda1", str(G / "vector4.omtf"), "--graph",
                                   str(G / "triangle.json")])
-    assert r.exit_code == 2 and "not found" in r.output
-    r = CliRunner().invoke(main, ["solve", "vector", "--lambda0", str(G / "vector4.omtf"),
+    assert code == 2 and "not found" in output
+    code, output = _cli(["solve", "vector", "--lambda0", str(G / "vector4.omtf"),
                                   "--lambda1", str(G / "vector4.omtf")])
-    assert r.exit_code == 2 and "--graph" in r.output
-    r = CliRunner().invoke(main, ["solve", "matrix", "--lambda0", str(G / "vector4.omtf"),
+    assert code == 2 and "--graph" in output
+    code, output = _cli(["solve", "matrix", "--lambda0", str(G / "vector4.omtf"),
                                   "--lambda1", str(G / "vector4.omtf"), "--lindblad",
                                   str(G / "lindblad3.json")])
-    assert r.exit_code == 2
-    r = CliRunner().invoke(main, ["bench", "--suite", "vector", "--sizes", ",",
+    assert code == 2
+    code, output = _cli(["bench", "--suite", "vector", "--sizes", ",",
                                   "--out", str(tmp_path / "t.csv")])
-    assert r.exit_code == 2
+    assert code == 2
 
 
 def test_graph_info():
-    r = CliRunner().invoke(main, ["graph-info", "--graph", str(G / "triangle.json")])
-    assert r.exit_code == 0
-    assert "nodes: 3, edges: 3" in r.output and "lambda_max" in r.output
+    code, output = _cli(["graph-info", "--graph", str(G / "triangle.json")])
+    assert code == 0
+    assert "nodes: 3, edges: 3" in output and "lambda_max" in output

@@ -1,0 +1,128 @@
+"""Channel and Lindblad counts beyond the common cases: the reference's
+TransportGraph (S/graph.py:23-70) takes any connected graph on k nodes and its
+LindbladSet (S/lindblad.py:47-66) any ell Hermitian k x k matrices with a
+nondegenerate gradient.  The engine instantiates vector payloads for
+k = 2..8 and matrix payloads for k = 2..4 with ell <= 4, and k = 2, 3 with
+ell <= 8 (the eight Gell-Mann matrices of su(3)); each is checked here against
+the oracle through every execution path, and what lies outside is rejected
+with UnsupportedNormError before any device work."""
+
+import numpy as np
+import pytest
+
+import gpu_util as g
+import paper_1712_10279_b200 as pk
+from oracle import pdhg
+
+pytestmark = pytest.mark.gpu
+
+PATHS = {"default": {}, "register": {"OTFX_CLUSTER": "0", "OTFX_TMA": "0"},
+         "tma": {"OTFX_TMA": "1"}}
+
+
+def _norm(rng, shape):
+    v = rng.random(shape) + 0.05
+    return v / v.sum()
+
+
+def gell_mann():
+    """The eight Gell-Mann matrices (a basis of su(3))."""
+    m = np.zeros((8, 3, 3), dtype=np.complex128)
+    pairs = [(0, 1), (0, 2), (1, 2)]
+    s = 0
+    for a, b in pairs:
+        m[s, a, b] = m[s, b, a] = 1.0
+        s += 1
+        m[s, a, b], m[s, b, a] = -1j, 1j
+        s += 1
+    m[6] = np.diag([1.0, -1.0, 0.0])
+    m[7] = np.diag([1.0, 1.0, -2.0]) / np.sqrt(3.0)
+    return m
+
+
+def _psd(rng, n, k, complex_):
+    a = rng.normal(size=(n, n, k, k))
+    if complex_:
+        a = a + 1j * rng.normal(size=(n, n, k, k))
+    p = a @ np.conj(np.swapaxes(a, -1, -2))
+    return (p / np.sum(np.real(np.trace(p, axis1=2, axis2=3)))).astype(np.complex128)
+
+
+def _check(rep, st, eng, iters, ce, bit_exact):
+    _, _, hist = pdhg.oracle_run(eng, 1e-300, 1e-300, iters, ce)
+    assert rep.iterations == iters
+    g.hist_close(g.hist_array(rep), np.array(hist), 1e-10)
+    assert g.rel_err(st.phi, eng.phi) <= 1e-10
+    assert g.rel_err(st.u.ux, eng.u[:, :, 0]) <= 1e-10
+    assert g.rel_err(st.u.uy, eng.u[:, :, 1]) <= 1e-10
+    assert g.rel_err(st.w.values, eng.w) <= 1e-10
+    if bit_exact:
+        assert np.array_equal(st.phi, eng.phi) and np.array_equal(st.w.values, eng.w)
+
+
+@pytest.mark.parametrize("path", sorted(PATHS))
+@pytest.mark.parametrize("k,graph_kind", [(7, "chain"), (7, "complete"), (8, "star"), (5, "chain")])
+def test_vector_channel_counts(monkeypatch, path, k, graph_kind):
+    for key, val in PATHS[path].items():
+        monkeypatch.setenv(key, val)
+    rng = np.random.default_rng(k * 10 + len(graph_kind))
+    if graph_kind == "chain":
+        edges = [(c, c + 1) for c in range(k - 1)]
+    elif graph_kind == "star":
+        edges = [(0, c) for c in range(1, k)]
+    else:
+        edges = [(a, b) for a in range(k) for b in range(a + 1, k)]
+    graph = pk.TransportGraph(k, edges, rng.uniform(0.5, 2.0, len(edges)))
+    n, iters, ce, tau, alpha = 40, 60, 20, 3.0, 0.05
+    l0, l1 = _norm(rng, (n, n, k)), _norm(rng, (n, n, k))
+    cfg = pk.SolverConfig(tau=tau, norm_u="l12", norm_w="l1", alpha=alpha, tol_gap=1e-300,
+                          tol_feas=1e-300, max_iters=iters, check_every=ce)
+    rep, st = pk.solve_vector(pk.VectorDensity(l0), pk.VectorDensity(l1), graph, cfg=cfg)
+    eng = pdhg.OracleEngine("vector", l0 - l1, n, tau, norm_u="l12", norm_w="l1", alpha=alpha,
+                            chan=graph.coefficients(), lam_chan=pk.lambda_max_graph(graph))
+    assert np.count_nonzero(st.w.values) > 0  # the channel flux is active
+    _check(rep, st, eng, iters, ce, bit_exact=False)
+
+
+@pytest.mark.parametrize("path", sorted(PATHS))
+@pytest.mark.parametrize("case", ["gellmann_l2l1", "gellmann_nuc", "k2_ell6_real", "k3_ell5_real"])
+def test_matrix_lindblad_counts(monkeypatch, path, case):
+    for key, val in PATHS[path].items():
+        monkeypatch.setenv(key, val)
+    rng = np.random.default_rng(len(case))
+    n, iters, ce, tau, alpha = 24, 40, 20, 10.0, 0.3
+    if case.startswith("gellmann"):
+        k, mats, cplx = 3, gell_mann(), True
+        nu, nw = ("l1nuc", "l1nuc") if case.endswith("nuc") else ("l2", "l1")
+    else:
+        k = 2 if case.startswith("k2") else 3
+        ell = 6 if k == 2 else 5
+        a = rng.normal(size=(ell, k, k))
+        mats, cplx = 0.5 * (a + np.swapaxes(a, -1, -2)), False
+        nu, nw = "l2", "l1"
+    lind = pk.LindbladSet(mats)
+    assert lind.ell > 4
+    l0, l1 = _psd(rng, n, k, cplx), _psd(rng, n, k, cplx)
+    cfg = pk.SolverConfig(tau=tau, norm_u=nu, norm_w=nw, alpha=alpha, tol_gap=1e-300,
+                          tol_feas=1e-300, max_iters=iters, check_every=ce)
+    rep, st = pk.solve_matrix(pk.MatrixDensity(l0), pk.MatrixDensity(l1), lind, cfg=cfg)
+    real_path = st.phi.dtype == np.float64
+    assert real_path == (not cplx)
+    dt = np.float64 if real_path else np.complex128
+    diff = (l0 - l1).real if real_path else (l0 - l1)
+    chan = lind.matrices.real if real_path else lind.matrices
+    eng = pdhg.OracleEngine("matrix", diff.astype(dt), n, tau, norm_u=nu, norm_w=nw, alpha=alpha,
+                            chan=chan, lam_chan=pk.lambda_max_L(lind), dtype=dt)
+    assert st.w.values.dtype == dt  # real path: float64 w, as the reference
+    _check(rep, st, eng, iters, ce, bit_exact=False)
+
+
+def test_outside_the_instantiations_is_rejected():
+    rng = np.random.default_rng(0)
+    n = 8
+    k = 9
+    graph = pk.TransportGraph(k, [(c, c + 1) for c in range(k - 1)], np.ones(k - 1))
+    l0, l1 = _norm(rng, (n, n, k)), _norm(rng, (n, n, k))
+    with pytest.raises(pk.UnsupportedNormError):
+        pk.solve_vector(pk.VectorDensity(l0), pk.VectorDensity(l1), graph,
+                        cfg=pk.SolverConfig(max_iters=10))

@@ -2,16 +2,25 @@
 outputs (S/cli.py:160-357) produced by the B200 engine."""
 
 import csv
+import contextlib
+import io
 import json
 from pathlib import Path
 
 import numpy as np
 import pytest
-from click.testing import CliRunner
 
 import paper_1712_10279_b200 as pk
 from paper_1712_10279_b200 import omtf, synthetic
 from paper_1712_10279_b200.cli import main
+
+
+def _cli(args):
+    """Run the CLI in-process: (exit code, stdout + stderr)."""
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf), contextlib.redirect_stderr(buf):
+        code = main([str(a) for a in args])
+    return code, buf.getvalue()
 
 pytestmark = pytest.mark.gpu
 G = Path(__file__).resolve().parent / "golden" / "omtf"
@@ -19,9 +28,9 @@ G = Path(__file__).resolve().parent / "golden" / "omtf"
 
 def test_cli_bench_vector_matches_api(tmp_path):
     out = tmp_path / "t.csv"
-    r = CliRunner().invoke(main, ["bench", "--suite", "vector", "--sizes", "16,24",
+    code, output = _cli(["bench", "--suite", "vector", "--sizes", "16,24",
                                   "--max-iters", "700", "--out", str(out)])
-    assert r.exit_code == 0, r.output
+    assert code == 0, output
     rows = list(csv.DictReader(open(out)))
     assert list(rows[0].keys()) == ["n", "iterations", "time_per_iter_s", "total_time_s", "tau",
                                     "transport_value"]
@@ -35,9 +44,9 @@ def test_cli_bench_vector_matches_api(tmp_path):
 
 def test_cli_bench_matrix(tmp_path):
     out = tmp_path / "m.csv"
-    r = CliRunner().invoke(main, ["bench", "--suite", "matrix", "--sizes", "8",
+    code, output = _cli(["bench", "--suite", "matrix", "--sizes", "8",
                                   "--out", str(out)])
-    assert r.exit_code == 0, r.output
+    assert code == 0, output
     rows = list(csv.DictReader(open(out)))
     assert float(rows[0]["tau"]) == 10.0 and int(rows[0]["iterations"]) > 0
 
@@ -50,22 +59,22 @@ def test_cli_solve_artifacts(tmp_path):
             str(tmp_path / "b.omtf"), "--graph", str(G / "triangle.json"), "--tau", "3",
             "--out-metrics", str(tmp_path / "m.json"), "--out-flux", str(tmp_path / "flux"),
             "--out-quiver", str(tmp_path / "q.csv")]
-    r = CliRunner().invoke(main, args)
-    assert r.exit_code == 0, r.output
+    code, output = _cli(args)
+    assert code == 0, output
     m = json.loads((tmp_path / "m.json").read_text())
     assert m["converged"] and m["config"]["tau"] == 3.0 and m["kind"] == "vector"
     assert (tmp_path / "flux.ux.omtf").read_bytes()[:5] == b"OMTF1"
     assert sum(1 for _ in open(tmp_path / "q.csv")) == 1 + 3 * 12 * 12
     # non-convergence -> exit 1
-    r = CliRunner().invoke(main, args[:-6] + ["--max-iters", "3"])
-    assert r.exit_code == 1
+    code, output = _cli(args[:-6] + ["--max-iters", "3"])
+    assert code == 1
 
 
 def test_cli_solve_matrix_from_reference_files(tmp_path):
     m = omtf.read_omtf(G / "matrix_real6.omtf")
     omtf.write_omtf(tmp_path / "b.omtf", pk.MatrixDensity(m.values[:, ::-1].copy()))
-    r = CliRunner().invoke(main, ["solve", "matrix", "--lambda0", str(G / "matrix_real6.omtf"),
+    code, output = _cli(["solve", "matrix", "--lambda0", str(G / "matrix_real6.omtf"),
                                   "--lambda1", str(tmp_path / "b.omtf"), "--lindblad",
                                   str(G / "lindblad3.json"), "--tau", "10", "--max-iters", "500"])
-    assert r.exit_code in (0, 1), r.output
-    assert "matrix: value=" in r.output
+    assert code in (0, 1), output
+    assert "matrix: value=" in output
