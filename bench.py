@@ -314,11 +314,9 @@ def run_ours(args):
     last = (hist[-1].primal, hist[-1].dual, hist[-1].gap_ratio)
     ms = start.elapsed_time(stop)
     plain_ms, plain_iters = eng.timing(0)
-    # with temporal blocking one launch (one HBM pass) advances two iterations
-    ipl = 2 if info["tb2"] else 1
-    sweep_ms = plain_ms / max(plain_iters / ipl, 1)
+    sweep_ms = plain_ms / max(plain_iters, 1)
     if not sweep_ms > 0:  # no plain iterations timed: fall back to the whole step
-        sweep_ms = ms / max(args.steps * ips / ipl, 1)
+        sweep_ms = ms / max(args.steps * ips, 1)
     t = torch.tensor([ms, sweep_ms], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -370,21 +368,16 @@ def run_ours(args):
                 "tile": [info["tile_cols"], info["tile_rows"]],
                 "regs": [info["regs_plain"], info["regs_check"]],
                 "tma_stages": info["tma_stages"], "smem_per_cta": info["smem_bytes"],
-                "temporal_blocking": bool(info["tb2"]), "regs_tb2": info["regs_tb2"],
-                "smem_per_cta_tb2": info["smem_tb2"],
                 "final_primal": last[0], "final_gap": last[2]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("sweep_tb2_kernel (two PDHG iterations per HBM pass)"
-                                    if info["tb2"] else
-                                    "sweep_tma_kernel (TMA-streamed fused PDHG iteration)"
+                         "kernel": ("sweep_tma_kernel (TMA-streamed fused PDHG iteration)"
                                     if info["tma_stages"] else
                                     "sweep_kernel (register-streamed fused PDHG iteration)"),
-                         "iterations_per_launch": ipl,
+                         "iterations_per_launch": 1,
                          "bytes_per_launch": balg, "avg_launch_ms": sweep_ms,
-                         # whole-step compulsory bandwidth: (iterations per pass) x HBM bytes
-                         "step_frac": value / world * bytes_per_cell(args.precision) / ipl
-                                      / 1e9 / peak,
+                         # whole-step compulsory bandwidth (checks included)
+                         "step_frac": value / world * bytes_per_cell(args.precision) / 1e9 / peak,
                          "effective_gbs_per_iteration": value / world
                                                         * bytes_per_cell(args.precision) / 1e9,
                          "peak_source": peak_src},
@@ -595,7 +588,7 @@ def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn):
         t0 = time.perf_counter()
         rep, st = call()
         times.append(time.perf_counter() - t0)
-    t = torch.tensor([max(times) if False else float(np.mean(times))], device="cuda")
+    t = torch.tensor([float(np.mean(times))], device="cuda")
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         comm.close()  # every rank, same point

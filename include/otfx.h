@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define OTFX_ABI_VERSION 1
+#define OTFX_ABI_VERSION 2
 
 /* error codes; the Python layer maps them onto the reference's exceptions
  * (S/errors.py:4-21) */
@@ -112,9 +112,6 @@ typedef struct {
   int32_t graphs;        /* CUDA graphs in use */
   int32_t tma_stages;    /* TMA ring depth of the streamed sweep (0: register sweep) */
   int32_t smem_bytes;    /* dynamic shared memory per sweep CTA */
-  int32_t tb2;           /* plain iterations run two per HBM pass (temporal blocking) */
-  int32_t regs_tb2;      /* registers per thread of the two-level sweep */
-  int32_t smem_tb2;      /* dynamic shared memory per two-level CTA */
   int32_t cluster_ctas;  /* > 0: run()/step() execute on chip in one cluster of this many CTAs */
   int32_t halo_overlap;  /* slab halo exchange overlapped with the interior bands when decomposed */
 } otfx_engine_info;
@@ -189,8 +186,12 @@ int otfx_engine_evaluate(otfx_engine* e, double out[4]);
 /* one iteration followed by R^k and evaluate (S/solver.py:305-313):
  * out = primal, dual, gap_ratio, feas, residual */
 int otfx_engine_step_check(otfx_engine* e, double out[5]);
-/* the whole _run loop (S/solver.py:294-337) on the device; history must hold
- * max_iters/check_every + 2 points */
+/* the whole _run loop (S/solver.py:294-337) on the device.  The engine keeps
+ * the run's whole history (the reference grows its list as it goes,
+ * S/solver.py:300-333); the first `capacity` points are copied to `history`
+ * (which may be NULL when capacity is 0) and n_history is the total, so a
+ * caller whose buffer was too small fetches the rest with
+ * otfx_engine_history. */
 int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_point* history,
                     int64_t capacity, int64_t* n_history, int64_t* iterations, int* converged,
                     double* wall_seconds);
@@ -205,6 +206,11 @@ int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_poi
 int otfx_engines_run_local(otfx_engine* const* engines, int count, const otfx_run_config* cfg,
                            otfx_history_point* history, int64_t capacity, int64_t* n_history,
                            int64_t* iterations, int* converged);
+
+/* the history of the engine's last run (for a local slab group: the lead
+ * engine's): the first `capacity` points into `history`, n_history = total */
+int otfx_engine_history(otfx_engine* e, otfx_history_point* history, int64_t capacity,
+                        int64_t* n_history);
 
 /* fixed-point residual between two given iterates (residual_Rk,
  * S/solver.py:501-526), using the engine's mu, nu, tau; whole-grid engines */

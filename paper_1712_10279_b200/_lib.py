@@ -49,7 +49,6 @@ class EngineInfo(C.Structure):
                 ("tile_cols", C.c_int32), ("tile_rows", C.c_int32), ("grid_x", C.c_int32),
                 ("grid_y", C.c_int32), ("regs_plain", C.c_int32), ("regs_check", C.c_int32),
                 ("graphs", C.c_int32), ("tma_stages", C.c_int32), ("smem_bytes", C.c_int32),
-                ("tb2", C.c_int32), ("regs_tb2", C.c_int32), ("smem_tb2", C.c_int32),
                 ("cluster_ctas", C.c_int32), ("halo_overlap", C.c_int32)]
 
 
@@ -83,6 +82,8 @@ SIGNATURES = {
                                          C.POINTER(HistoryPointC), C.c_int64,
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int)]),
+    "otfx_engine_history": (C.c_int, [_P, C.POINTER(HistoryPointC), C.c_int64,
+                                      C.POINTER(C.c_int64)]),
     "otfx_engine_residual_between": (C.c_int, [_P] + [_P] * 8 + [_DP]),
     "otfx_engine_sweep": (C.c_int, [_P, C.c_int]),
     "otfx_engine_raw": (C.c_int, [_P, C.c_int, _DP]),

@@ -320,13 +320,11 @@ struct otfx_engine {
   cudaEvent_t ev_hand = nullptr;  // caller-stream ordering of the device hand-off
   // TMA-streamed sweep
   bool use_tma = false;
+  // history of the last run() (the caller's buffer may be smaller: it gets
+  // the first `capacity` rows, otfx_engine_history returns all of them)
+  std::vector<otfx_history_point> history;
   otfx::StageLayout L{};
   otfx::TmaSet maps[2];
-  // temporal blocking: two iterations per pass (single-slab engines)
-  bool use_tb2 = false;
-  otfx::StageLayout L2{};
-  otfx::TmaSet maps2[2];
-  int gx2 = 1, gy2 = 1;
   // on-chip cluster solve (small single-slab grids)
   bool use_cluster = false;
   int cl_ctas = 0, cl_threads = 0, cl_rows = 0;
@@ -496,50 +494,9 @@ static bool plan_stages(otfx_engine* e, int S) {
   return L.total <= 227 * 1024;
 }
 
-// shared-memory plan of the two-level sweep (same formulas as TB2Shape<P,T>)
-static bool plan_tb2(otfx_engine* e, int S) {
-  StageLayout& L = e->L2;
-  require(S >= 3 && S <= 8, OTFX_EINVAL, "TMA ring depth must be in [3, 8]");
-  L.cw = 4;
-  L.tile = 29 * 4;
-  L.h = 16 / e->elem;
-  L.tw = ((118 + L.h) + L.h - 1) / L.h * L.h;
-  L.S = S;
-  const int row = L.tw * e->elem;
-  const int bu = 2 * e->NP * row, bw = e->NWact * row, bd = e->NP * row, bp = e->NP * row;
-  const int nwcap = e->has_w ? e->LMAX * e->NWS : 1;
-  L.off_w = round_up(bu, 128);
-  L.off_d = L.off_w + round_up(nwcap * row, 128);
-  L.off_p = L.off_d + round_up(bd, 128);
-  L.stage_bytes = L.off_p + round_up(bp, 128);
-  L.bytes_full = bu + bw + bd + bp;
-  L.bytes_flux = bu + bp;
-  L.bytes_phi = bp;
-  L.off_stages = 128;
-  L.off_xchg = L.off_stages + S * L.stage_bytes;
-  L.off_red = round_up(L.off_xchg, 16);
-  L.total = L.off_red;
-  return L.total <= 227 * 1024;
-}
-
 static void launch_sweep(otfx_engine* e, int fl) {
   if (e->elem == 8) launch_sweep<double>(e, fl);
   else launch_sweep<float>(e, fl);
-}
-
-// two plain iterations in one pass (sweep_tb2_kernel)
-template <typename T>
-static void launch_tb2(otfx_engine* e) {
-  TmaSweepArgs<T> g;
-  g.s = make_args<T>(e, e->cur);
-  g.L = e->L2;
-  CK(ops_of<T>(e)->sweep_tb2(g, e->maps2[e->cur], dim3(e->gx2, e->gy2), dim3(160), e->stream));
-  e->cur ^= 1;
-}
-
-static void launch_tb2(otfx_engine* e) {
-  if (e->elem == 8) launch_tb2<double>(e);
-  else launch_tb2<float>(e);
 }
 
 template <typename T>
@@ -685,7 +642,7 @@ static void exchange_nccl(otfx_engine* e) { exchange_nccl(e, e->stream); }
 // no interior band touches.  The engine stream then joins the edge stream, so
 // the exchange of iteration k is hidden behind the interior of iteration k.
 static bool overlap_ready(const otfx_engine* e) {
-  return e->gy >= 3 && !e->use_tb2 && env_int("OTFX_OVERLAP", 1) != 0;
+  return e->gy >= 3 && env_int("OTFX_OVERLAP", 1) != 0;
 }
 
 static void ensure_overlap(otfx_engine* e) {
@@ -725,16 +682,7 @@ static void sweep_exchange(otfx_engine* e, int fl) {
 }
 
 static void enqueue_plain(otfx_engine* e, int64_t count) {
-  int64_t q = 0;
-  if (e->use_tb2) {
-    for (; q + 2 <= count; q += 2) launch_tb2(e);
-  }
-  for (; q < count; ++q) sweep_exchange(e, 0);
-}
-
-// buffer flips of enqueue_plain(count)
-static int64_t plain_flips(const otfx_engine* e, int64_t count) {
-  return e->use_tb2 ? count / 2 + count % 2 : count;
+  for (int64_t q = 0; q < count; ++q) sweep_exchange(e, 0);
 }
 
 // device-time bracket (CUDA events on the engine stream) around a run of
@@ -793,7 +741,7 @@ static void run_plain(otfx_engine* e, int64_t count) {
   const int slot = timing_begin(e);
   CK(cudaGraphLaunch(it->second, e->stream));
   timing_end(e, slot, count);
-  e->cur ^= int(plain_flips(e, count) & 1);
+  e->cur ^= int(count & 1);
 }
 
 // fold the timed graph launches into plain_ms once the stream has caught up
@@ -1468,12 +1416,6 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     }
     e->use_tma = plan_stages(e, std::max(smin, S));
   }
-  // two-level sweep (temporal blocking), opt-in with OTFX_TB2=1: on B200 in fp64
-  // it is bound by the dependent DP chains (2x the instructions per pass at
-  // ~50 % issue), so two single sweeps are faster; see profiles/README.md
-  const bool tb2_inst = e->ops64 ? e->ops64->sweep_tb2 != nullptr : e->ops32->sweep_tb2 != nullptr;
-  e->use_tb2 = e->use_tma && tb2_inst && e->rows == n && env_int("OTFX_TB2", 0) != 0 &&
-               plan_tb2(e, env_int("OTFX_TB2_STAGES", 4));
   if (e->use_tma) {
     e->gx = (n + e->L.tile - 1) / e->L.tile;
     // Row split.  Short CTAs (16 rows) keep the set of CTAs resident at any
@@ -1505,10 +1447,6 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     }
     e->R = env_int("OTFX_TILE_ROWS", R);
     e->gy = (e->rows + e->R - 1) / e->R;
-  }
-  if (e->use_tb2) {
-    e->gx2 = (n + e->L2.tile - 1) / e->L2.tile;
-    e->gy2 = e->gy;
   }
 
   // On-chip solve: a small single-slab grid whose state fits in the shared
@@ -1595,14 +1533,6 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
       make_map(e, &e->maps[st].w, e->w[st], e->NWact, e->L.tw);
       make_map(e, &e->maps[st].phi, e->phi[st], NP, e->L.tw);
       make_map(e, &e->maps[st].diff, e->diff, NP, e->L.tw);
-    }
-  }
-  if (e->use_tb2) {
-    for (int st = 0; st < 2; ++st) {
-      make_map(e, &e->maps2[st].u, e->u[st], 2 * NP, e->L2.tw);
-      make_map(e, &e->maps2[st].w, e->w[st], e->NWact, e->L2.tw);
-      make_map(e, &e->maps2[st].phi, e->phi[st], NP, e->L2.tw);
-      make_map(e, &e->maps2[st].diff, e->diff, NP, e->L2.tw);
     }
   }
   CK(cudaMallocHost(&e->h_raw, 64 * sizeof(double)));
@@ -1735,6 +1665,16 @@ static void group_raw(const SlabGroup& g, bool fused, bool with_res, double raw[
 }
 
 // the _run loop (S/solver.py:294-337) over a slab group
+// the first `capacity` rows of the engine's history into the caller's buffer;
+// n_history = all rows (more than capacity: fetch them with otfx_engine_history)
+static void copy_history(const otfx_engine* e, otfx_history_point* hist, int64_t capacity,
+                         int64_t* n_history) {
+  const int64_t nh = int64_t(e->history.size());
+  if (hist && capacity > 0)
+    std::copy(e->history.begin(), e->history.begin() + std::min(nh, capacity), hist);
+  *n_history = nh;
+}
+
 static void run_loop(const SlabGroup& g, const otfx_run_config* cfg, otfx_history_point* hist,
                      int64_t capacity, int64_t* n_history, int64_t* iterations, int* converged) {
   otfx_engine* e = g.lead();
@@ -1747,10 +1687,10 @@ static void run_loop(const SlabGroup& g, const otfx_run_config* cfg, otfx_histor
     for (int q = 0; q < g.count; ++q) s2 += g.es[q]->diff_norm_own * g.es[q]->diff_norm_own;
     dn = std::sqrt(s2);
   }
-  int64_t nh = 0;
+  std::vector<otfx_history_point>& H = e->history;
+  H.clear();
   auto push = [&](int64_t it, const double* r, double rk) {
-    require(nh < capacity, OTFX_EINVAL, "history buffer too small");
-    hist[nh++] = {double(it), r[0], r[1], r[2], r[3], rk};
+    H.push_back({double(it), r[0], r[1], r[2], r[3], rk});
   };
   double r[5], raw[OTFX_NRAW];
   group_raw(g, false, false, raw);
@@ -1785,7 +1725,7 @@ static void run_loop(const SlabGroup& g, const otfx_run_config* cfg, otfx_histor
       }
     }
   }
-  *n_history = nh;
+  copy_history(e, hist, capacity, n_history);
   *iterations = it;
   *converged = conv ? 1 : 0;
 }
@@ -1886,9 +1826,6 @@ int otfx_engine_get_info(otfx_engine* e, otfx_engine_info* info) {
   info->regs_check = e->ops64 ? e->ops64->sweep_regs(true) : e->ops32->sweep_regs(true);
   info->graphs = e->use_graphs ? 1 : 0;
   info->tma_stages = e->use_tma ? e->L.S : 0;
-  info->tb2 = e->use_tb2 ? 1 : 0;
-  info->regs_tb2 = e->use_tb2 ? (e->ops64 ? e->ops64->tb2_regs() : e->ops32->tb2_regs()) : 0;
-  info->smem_tb2 = e->use_tb2 ? e->L2.total : 0;
   info->smem_bytes = e->use_tma ? e->L.total : int(e->smem_plain);
   info->cluster_ctas = cluster_ok(e) ? e->cl_ctas : 0;
   info->halo_overlap = overlap_ready(e) ? 1 : 0;
@@ -2105,7 +2042,7 @@ int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_poi
                     int64_t capacity, int64_t* n_history, int64_t* iterations, int* converged,
                     double* wall_seconds) {
   API_BEGIN
-  require(e && cfg && hist && n_history && iterations && converged, OTFX_EINVAL, "null pointer");
+  require(e && cfg && n_history && iterations && converged, OTFX_EINVAL, "null pointer");
   require(cfg->max_iters >= 1 && cfg->check_every >= 1, OTFX_EINVAL,
           "max_iters and check_every must be >= 1");
   CK(cudaSetDevice(e->d.device));
@@ -2118,14 +2055,13 @@ int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_poi
     long long res[4];
     CK(cudaMemcpyAsync(res, e->d_result, sizeof(res), cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
-    require(res[1] >= 1 && res[1] <= capacity, OTFX_EINVAL, "history buffer too small");
-    std::vector<double> h(size_t(res[1]) * 6);
-    CK(cudaMemcpyAsync(h.data(), e->d_stage, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                       e->stream));
+    require(res[1] >= 1, OTFX_ECUDA, "on-chip solve returned no history");
+    e->history.resize(size_t(res[1]));
+    static_assert(sizeof(otfx_history_point) == 6 * sizeof(double), "history row layout");
+    CK(cudaMemcpyAsync(e->history.data(), e->d_stage, e->history.size() * sizeof(otfx_history_point),
+                       cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
-    for (long long q = 0; q < res[1]; ++q)
-      hist[q] = {h[q * 6], h[q * 6 + 1], h[q * 6 + 2], h[q * 6 + 3], h[q * 6 + 4], h[q * 6 + 5]};
-    *n_history = res[1];
+    copy_history(e, hist, capacity, n_history);
     *iterations = res[0];
     *converged = int(res[2]);
     e->residual_valid = false;
@@ -2143,7 +2079,7 @@ int otfx_engines_run_local(otfx_engine* const* es, int count, const otfx_run_con
                            otfx_history_point* hist, int64_t capacity, int64_t* n_history,
                            int64_t* iterations, int* converged) {
   API_BEGIN
-  require(es && count >= 1 && cfg && hist && n_history && iterations && converged, OTFX_EINVAL,
+  require(es && count >= 1 && cfg && n_history && iterations && converged, OTFX_EINVAL,
           "null pointer");
   require(cfg->max_iters >= 1 && cfg->check_every >= 1, OTFX_EINVAL,
           "max_iters and check_every must be >= 1");
@@ -2155,6 +2091,14 @@ int otfx_engines_run_local(otfx_engine* const* es, int count, const otfx_run_con
   }
   CK(cudaSetDevice(es[0]->d.device));
   run_loop(SlabGroup{es, count}, cfg, hist, capacity, n_history, iterations, converged);
+  API_END
+}
+
+int otfx_engine_history(otfx_engine* e, otfx_history_point* hist, int64_t capacity,
+                        int64_t* n_history) {
+  API_BEGIN
+  require(e && n_history, OTFX_EINVAL, "null pointer");
+  copy_history(e, hist, capacity, n_history);
   API_END
 }
 
@@ -2232,7 +2176,6 @@ int otfx_engine_attach_nccl(otfx_engine* e, const unsigned char id[128], int nra
   e->own_comm = true;
   e->nranks = nranks;
   e->rank = rank;
-  if (nranks > 1) e->use_tb2 = false;  // the two-level sweep needs depth-2 halos
   drop_graphs(e);
   API_END
 }
@@ -2277,7 +2220,6 @@ int otfx_engine_attach_comm(otfx_engine* e, otfx_comm* c) {
   e->own_comm = false;
   e->nranks = c->nranks;
   e->rank = c->rank;
-  if (c->nranks > 1) e->use_tb2 = false;
   drop_graphs(e);
   API_END
 }

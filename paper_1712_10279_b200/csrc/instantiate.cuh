@@ -4,7 +4,6 @@
 #include "ops.h"
 #include "sweep.cuh"
 #include "sweep_tma.cuh"
-#include "sweep_tb2.cuh"
 
 namespace otfx {
 
@@ -25,30 +24,7 @@ struct OpsFor {
       e = cudaFuncSetAttribute(tk[q], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       if (e != cudaSuccess) return e;
     }
-    if constexpr (TB2) {
-      return cudaFuncSetAttribute(sweep_tb2_kernel<P, T>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    }
     return cudaSuccess;
-  }
-  // temporal blocking is instantiated for the graph payloads with k <= 4
-  // (the matrix payloads would spill the two register-resident levels)
-  static constexpr bool TB2 = (P::NCOEF > 0 || !P::HAS_W) && P::K <= 4;
-  static cudaError_t sweep_tb2(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
-                               cudaStream_t s) {
-    if constexpr (TB2) {
-      sweep_tb2_kernel<P, T><<<g, b, a.L.total, s>>>(a, m);
-      return cudaGetLastError();
-    }
-    return cudaErrorNotSupported;
-  }
-  static int tb2_regs() {
-    if constexpr (TB2) {
-      cudaFuncAttributes at;
-      cudaFuncGetAttributes(&at, sweep_tb2_kernel<P, T>);
-      return at.numRegs;
-    }
-    return 0;
   }
   // wide CTAs (8 consumer warps, 248 columns) for the graph payloads.  The
   // fp64 complex-Hermitian payloads with K >= 3 run at ptxas' 255-register cap,
@@ -175,7 +151,7 @@ struct OpsFor {
   static const Ops<T>* table(int kind) {
     static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
                              P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &sweep_tma,
-                             TB2 ? &sweep_tb2 : nullptr, &regs, &tma_regs, &tb2_regs,
+                             &regs, &tma_regs,
                              WIDE,     &tma_occupancy, &sweep_occupancy,
                              CLUSTER ? &cluster_run : nullptr, &cluster_smem, &cluster_fits};
     return &o;

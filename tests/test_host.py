@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
     assert set(names) <= set(_lib.SIGNATURES), set(names) - set(_lib.SIGNATURES)
-    assert _lib.load().otfx_abi_version() == 1
+    assert _lib.load().otfx_abi_version() == 2
 
 
 def test_error_codes_map_to_reference_exceptions():
