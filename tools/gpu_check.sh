@@ -1,7 +1,7 @@
-set -x
+# full GPU suite, smoke, bench (both arms); logs in gpurun_out/
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 2400 python -m pytest tests -m gpu -q -x --durations=25 > gpurun_out/gputest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gputest.log
+timeout 2400 python -m pytest tests -m gpu -q -x --durations=15 > gpurun_out/gputest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gputest.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1
-timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
-tail -3 gpurun_out/gputest.log; tail -2 gpurun_out/bench.log
+[ -n "$WITH_REF" ] && timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
+tail -3 gpurun_out/gputest.log; tail -c 600 gpurun_out/bench.log
