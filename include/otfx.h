@@ -207,6 +207,19 @@ int otfx_engines_run_local(otfx_engine* const* engines, int count, const otfx_ru
                            otfx_history_point* history, int64_t capacity, int64_t* n_history,
                            int64_t* iterations, int* converged);
 
+/* the same local slab group with the halo transport and the check-scalar
+ * allreduces going through NCCL: `loopback` is a one-rank communicator
+ * (otfx_comm_create with nranks = 1) on the slabs' device, and every halo
+ * send / receive of exchange_nccl is posted to that rank itself -- the same
+ * ncclSend / ncclRecv / ncclAllReduce calls, buffers, counts and datatypes the
+ * multi-GPU ranks post, executed on a one-GPU machine.  NULL = device copies
+ * (otfx_engines_run_local). */
+typedef struct otfx_comm otfx_comm;
+int otfx_engines_run_local_nccl(otfx_engine* const* engines, int count, otfx_comm* loopback,
+                                const otfx_run_config* cfg, otfx_history_point* history,
+                                int64_t capacity, int64_t* n_history, int64_t* iterations,
+                                int* converged);
+
 /* the history of the engine's last run (for a local slab group: the lead
  * engine's): the first `capacity` points into `history`, n_history = total */
 int otfx_engine_history(otfx_engine* e, otfx_history_point* history, int64_t capacity,
@@ -240,7 +253,6 @@ int otfx_engine_attach_nccl(otfx_engine* e, const unsigned char id[128], int nra
 /* a communicator that outlives engines: created once per process and rank,
  * attached (non-owning) to every engine of a series of solves, so the NCCL
  * setup is paid once rather than per solve */
-typedef struct otfx_comm otfx_comm;
 int otfx_comm_create(const unsigned char id[128], int nranks, int rank, int device,
                      otfx_comm** out);
 int otfx_comm_destroy(otfx_comm* c);

@@ -82,6 +82,10 @@ SIGNATURES = {
                                          C.POINTER(HistoryPointC), C.c_int64,
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int)]),
+    "otfx_engines_run_local_nccl": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, _P,
+                                              C.POINTER(RunConfig), C.POINTER(HistoryPointC),
+                                              C.c_int64, C.POINTER(C.c_int64),
+                                              C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
     "otfx_engine_history": (C.c_int, [_P, C.POINTER(HistoryPointC), C.c_int64,
                                       C.POINTER(C.c_int64)]),
     "otfx_engine_residual_between": (C.c_int, [_P] + [_P] * 8 + [_DP]),

@@ -755,45 +755,50 @@ static void collect_timing(otfx_engine* e) {
   e->ev_pending.clear();
 }
 
-// raw scalars of the current iterate into d_raw (and h_raw after sync)
-static void raw_to_host(otfx_engine* e, bool with_res, bool allreduce) {
-  launch_evaluate(e);
-  reduce_raw_kernel<<<1, 256, 0, e->stream>>>(e->d_part_eval, e->d_max_eval, e->ex * e->ey,
-                                               e->d_part_sweep, e->gx * e->gy, with_res ? 1 : 0,
-                                               e->d_raw);
-  CK(cudaGetLastError());
-  if (allreduce && e->comm && e->nranks > 1) {
-    NcclApi& N = nccl();
-    NK(N.GroupStart());
-    NK(N.AllReduce(e->d_raw, e->d_raw, OTFX_NRAW_SUM, ncclFloat64, ncclSum, e->comm, e->stream));
-    NK(N.AllReduce(e->d_raw + OTFX_NRAW_SUM, e->d_raw + OTFX_NRAW_SUM, OTFX_NRAW - OTFX_NRAW_SUM,
-                   ncclFloat64, ncclMax, e->comm, e->stream));
-    NK(N.GroupEnd());
-  }
+// SUM over the 12 sums, MAX over the two dual-norm maxima of d_raw, across
+// the ranks of `comm` (the engine's own communicator, or for a local slab
+// group the one-rank loopback communicator that exercises the same calls)
+static void allreduce_raw(otfx_engine* e, ncclComm_t comm) {
+  if (!comm) return;
+  NcclApi& N = nccl();
+  NK(N.GroupStart());
+  NK(N.AllReduce(e->d_raw, e->d_raw, OTFX_NRAW_SUM, ncclFloat64, ncclSum, comm, e->stream));
+  NK(N.AllReduce(e->d_raw + OTFX_NRAW_SUM, e->d_raw + OTFX_NRAW_SUM, OTFX_NRAW - OTFX_NRAW_SUM,
+                 ncclFloat64, ncclMax, comm, e->stream));
+  NK(N.GroupEnd());
+}
+
+static ncclComm_t rank_comm(const otfx_engine* e) {
+  return e->comm && e->nranks > 1 ? e->comm : nullptr;
+}
+
+static void raw_download(otfx_engine* e) {
   CK(cudaMemcpyAsync(e->h_raw, e->d_raw, OTFX_NRAW * sizeof(double), cudaMemcpyDeviceToHost,
                      e->stream));
   CK(cudaStreamSynchronize(e->stream));
   collect_timing(e);
 }
 
+// raw scalars of the current iterate into d_raw (and h_raw after sync),
+// allreduced over `ar` (nullptr: this engine's rows only)
+static void raw_to_host(otfx_engine* e, bool with_res, ncclComm_t ar) {
+  launch_evaluate(e);
+  reduce_raw_kernel<<<1, 256, 0, e->stream>>>(e->d_part_eval, e->d_max_eval, e->ex * e->ey,
+                                               e->d_part_sweep, e->gx * e->gy, with_res ? 1 : 0,
+                                               e->d_raw);
+  CK(cudaGetLastError());
+  allreduce_raw(e, ar);
+  raw_download(e);
+}
+
 // fused check: the check sweep already wrote R^k + primal/feasibility
 // partials, the speculative sweep after it the dual-norm partials
-static void raw_fused_to_host(otfx_engine* e) {
+static void raw_fused_to_host(otfx_engine* e, ncclComm_t ar) {
   reduce_fused_kernel<<<1, 256, 0, e->stream>>>(e->d_part_sweep, e->d_part_dual, e->gx * e->gy,
                                                  e->d_raw);
   CK(cudaGetLastError());
-  if (e->comm && e->nranks > 1) {
-    NcclApi& N = nccl();
-    NK(N.GroupStart());
-    NK(N.AllReduce(e->d_raw, e->d_raw, OTFX_NRAW_SUM, ncclFloat64, ncclSum, e->comm, e->stream));
-    NK(N.AllReduce(e->d_raw + OTFX_NRAW_SUM, e->d_raw + OTFX_NRAW_SUM, OTFX_NRAW - OTFX_NRAW_SUM,
-                   ncclFloat64, ncclMax, e->comm, e->stream));
-    NK(N.GroupEnd());
-  }
-  CK(cudaMemcpyAsync(e->h_raw, e->d_raw, OTFX_NRAW * sizeof(double), cudaMemcpyDeviceToHost,
-                     e->stream));
-  CK(cudaStreamSynchronize(e->stream));
-  collect_timing(e);
+  allreduce_raw(e, ar);
+  raw_download(e);
 }
 
 // ---- device memory pool ------------------------------------------------------
@@ -1597,6 +1602,7 @@ namespace otfx {
 struct SlabGroup {
   otfx_engine* const* es;
   int count;
+  ncclComm_t loop = nullptr;  // one-rank NCCL loopback transport (local groups)
   bool local() const { return count > 1; }
   otfx_engine* lead() const { return es[0]; }
 };
@@ -1604,7 +1610,8 @@ struct SlabGroup {
 // the slabs of one grid in one process: same pack / unpack as exchange_nccl,
 // the transport is a device copy of each send buffer into the neighbour's
 // receive buffer (what ncclSend/ncclRecv move between ranks)
-static void exchange_local_impl(otfx_engine* const* es, int count, cudaStream_t st) {
+static void exchange_local_impl(otfx_engine* const* es, int count, cudaStream_t st,
+                                ncclComm_t loop = nullptr) {
   for (int s = 0; s + 1 < count; ++s) {
     otfx_engine* a = es[s];
     otfx_engine* b = es[s + 1];
@@ -1615,12 +1622,32 @@ static void exchange_local_impl(otfx_engine* const* es, int count, cudaStream_t 
     require(a->cur == b->cur, OTFX_EINVAL, "engines are at different iterations");
   }
   for (int s = 0; s < count; ++s) halo_pack(es[s], s > 0, s + 1 < count, st);
-  for (int s = 0; s + 1 < count; ++s) {
-    const HaloBufs ha = halo_bufs(es[s]), hb = halo_bufs(es[s + 1]);
-    const size_t wb = size_t(es[s]->d.n) * es[s]->elem;
-    const int NP = es[s]->NP;
-    CK(cudaMemcpyAsync(hb.recv_top, ha.send_bot, 3 * NP * wb, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpyAsync(ha.recv_bot, hb.send_top, NP * wb, cudaMemcpyDeviceToDevice, st));
+  if (loop) {
+    // NCCL loopback: the same ncclSend / ncclRecv calls (buffers, counts,
+    // datatype, one group) exchange_nccl posts between ranks, addressed to
+    // this process's own rank; sends and receives to one peer match in
+    // posting order, so each boundary posts (a -> b), then (b -> a)
+    NcclApi& N = nccl();
+    const ncclDataType_t dt = es[0]->elem == 8 ? ncclFloat64 : ncclFloat32;
+    NK(N.GroupStart());
+    for (int s = 0; s + 1 < count; ++s) {
+      const HaloBufs ha = halo_bufs(es[s]), hb = halo_bufs(es[s + 1]);
+      const size_t w = size_t(es[s]->d.n);
+      const int NP = es[s]->NP;
+      NK(N.Send(ha.send_bot, 3 * NP * w, dt, 0, loop, st));
+      NK(N.Recv(hb.recv_top, 3 * NP * w, dt, 0, loop, st));
+      NK(N.Send(hb.send_top, NP * w, dt, 0, loop, st));
+      NK(N.Recv(ha.recv_bot, NP * w, dt, 0, loop, st));
+    }
+    NK(N.GroupEnd());
+  } else {
+    for (int s = 0; s + 1 < count; ++s) {
+      const HaloBufs ha = halo_bufs(es[s]), hb = halo_bufs(es[s + 1]);
+      const size_t wb = size_t(es[s]->d.n) * es[s]->elem;
+      const int NP = es[s]->NP;
+      CK(cudaMemcpyAsync(hb.recv_top, ha.send_bot, 3 * NP * wb, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(ha.recv_bot, hb.send_top, NP * wb, cudaMemcpyDeviceToDevice, st));
+    }
   }
   for (int s = 0; s < count; ++s) halo_unpack(es[s], s > 0, s + 1 < count, st);
 }
@@ -1636,11 +1663,11 @@ static void group_sweep(const SlabGroup& g, int fl) {
   for (int q = 0; q < g.count; ++q) ov = ov && overlap_ready(g.es[q]);
   if (ov) {
     overlapped_sweep(g.es, g.count, fl,
-                     [&](cudaStream_t st) { exchange_local_impl(g.es, g.count, st); });
+                     [&](cudaStream_t st) { exchange_local_impl(g.es, g.count, st, g.loop); });
     return;
   }
   for (int q = 0; q < g.count; ++q) launch_sweep(g.es[q], fl);
-  exchange_local_impl(g.es, g.count, g.lead()->stream);
+  exchange_local_impl(g.es, g.count, g.lead()->stream, g.loop);
 }
 
 static void group_plain(const SlabGroup& g, int64_t count) {
@@ -1657,8 +1684,9 @@ static void group_raw(const SlabGroup& g, bool fused, bool with_res, double raw[
   for (int q = 0; q < OTFX_NRAW; ++q) raw[q] = 0.0;
   for (int s = 0; s < g.count; ++s) {
     otfx_engine* e = g.es[s];
-    if (fused) raw_fused_to_host(e);
-    else raw_to_host(e, with_res, !g.local());
+    const ncclComm_t ar = g.local() ? g.loop : rank_comm(e);
+    if (fused) raw_fused_to_host(e, ar);
+    else raw_to_host(e, with_res, ar);
     for (int q = 0; q < R_NSUM; ++q) raw[q] += e->h_raw[q];
     for (int q = R_NSUM; q < OTFX_NRAW; ++q) raw[q] = s ? std::max(raw[q], e->h_raw[q]) : e->h_raw[q];
   }
@@ -2004,7 +2032,7 @@ int otfx_engine_evaluate(otfx_engine* e, double out[4]) {
   API_BEGIN
   require(e && out, OTFX_EINVAL, "null pointer");
   CK(cudaSetDevice(e->d.device));
-  raw_to_host(e, false, true);
+  raw_to_host(e, false, rank_comm(e));
   double r[5];
   finalize(e, e->h_raw, r);
   for (int q = 0; q < 4; ++q) out[q] = r[q];
@@ -2016,7 +2044,7 @@ int otfx_engine_step_check(otfx_engine* e, double out[5]) {
   require(e && out, OTFX_EINVAL, "null pointer");
   CK(cudaSetDevice(e->d.device));
   sweep_exchange(e, 1);
-  raw_to_host(e, true, true);
+  raw_to_host(e, true, rank_comm(e));
   finalize(e, e->h_raw, out);
   API_END
 }
@@ -2026,7 +2054,7 @@ int otfx_engine_raw(otfx_engine* e, int with_residual, double raw[OTFX_NRAW]) {
   require(e && raw, OTFX_EINVAL, "null pointer");
   require(!with_residual || e->residual_valid, OTFX_EINVAL, "no check sweep since the last step");
   CK(cudaSetDevice(e->d.device));
-  raw_to_host(e, with_residual != 0, false);
+  raw_to_host(e, with_residual != 0, nullptr);
   for (int q = 0; q < OTFX_NRAW; ++q) raw[q] = e->h_raw[q];
   API_END
 }
@@ -2078,7 +2106,18 @@ int otfx_engine_run(otfx_engine* e, const otfx_run_config* cfg, otfx_history_poi
 int otfx_engines_run_local(otfx_engine* const* es, int count, const otfx_run_config* cfg,
                            otfx_history_point* hist, int64_t capacity, int64_t* n_history,
                            int64_t* iterations, int* converged) {
+  return otfx_engines_run_local_nccl(es, count, nullptr, cfg, hist, capacity, n_history,
+                                     iterations, converged);
+}
+
+int otfx_engines_run_local_nccl(otfx_engine* const* es, int count, otfx_comm* loop,
+                                const otfx_run_config* cfg, otfx_history_point* hist,
+                                int64_t capacity, int64_t* n_history, int64_t* iterations,
+                                int* converged) {
   API_BEGIN
+  if (loop)
+    require(loop->nranks == 1 && loop->device == es[0]->d.device, OTFX_EINVAL,
+            "the loopback communicator must be a one-rank communicator on the slabs' device");
   require(es && count >= 1 && cfg && n_history && iterations && converged, OTFX_EINVAL,
           "null pointer");
   require(cfg->max_iters >= 1 && cfg->check_every >= 1, OTFX_EINVAL,
@@ -2090,7 +2129,8 @@ int otfx_engines_run_local(otfx_engine* const* es, int count, const otfx_run_con
             OTFX_EINVAL, "engines must be the slabs of one grid, in order");
   }
   CK(cudaSetDevice(es[0]->d.device));
-  run_loop(SlabGroup{es, count}, cfg, hist, capacity, n_history, iterations, converged);
+  run_loop(SlabGroup{es, count, loop ? loop->comm : nullptr}, cfg, hist, capacity, n_history,
+           iterations, converged);
   API_END
 }
 

@@ -464,17 +464,21 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def run_local(engines, tol_gap, tol_feas, max_iters, check_every):
+def run_local(engines, tol_gap, tol_feas, max_iters, check_every, loopback=None):
     """The run loop over the row-slab engines of one grid on one device, in
-    lockstep with local halo copies (the single-GPU stand-in for NCCL ranks)."""
+    lockstep with local halo copies (the single-GPU stand-in for NCCL ranks).
+    loopback: a one-rank SlabCommunicator; the halo transport and the check
+    allreduces then go through NCCL send / recv / allreduce to that rank."""
     cap = _history_cap(max_iters, check_every)
     hist = (_lib.HistoryPointC * cap)()
     cfg = _lib.RunConfig(tol_gap, tol_feas, int(max_iters), int(check_every))
     nh, it, conv = C.c_int64(), C.c_int64(), C.c_int()
     arr = (C.c_void_p * len(engines))(*[e.handle for e in engines])
     lib = _lib.load()
-    _lib.check(lib.otfx_engines_run_local(arr, len(engines), C.byref(cfg), hist, cap,
-                                          C.byref(nh), C.byref(it), C.byref(conv)))
+    _lib.check(lib.otfx_engines_run_local_nccl(arr, len(engines),
+                                               loopback.handle if loopback else None,
+                                               C.byref(cfg), hist, cap, C.byref(nh),
+                                               C.byref(it), C.byref(conv)))
     history = _history(lib, engines[0].handle, hist, cap, nh.value)
     return history, it.value, bool(conv.value)
 

@@ -614,15 +614,22 @@ def test_pooled_engines_reuse_memory_and_release():
 # rule) over P row slabs of one grid on one GPU, with the TMA-streamed slab
 # sweeps the multi-GPU bench runs: same iterates and history as one engine
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("transport", ["copy", "nccl"])
 @pytest.mark.parametrize("overlap", ["1", "0"])
 @pytest.mark.parametrize("P,n,force_tma,conv", [
     (2, 300, True, False), (3, 301, True, False), (2, 1100, False, False), (2, 32, True, True),
     (4, 900, True, False),
 ])
-def test_local_slab_run_loop_matches_single_engine(monkeypatch, P, n, force_tma, conv, overlap):
+def test_local_slab_run_loop_matches_single_engine(monkeypatch, P, n, force_tma, conv, overlap,
+                                                   transport):
     """overlap=1: edge bands + halo exchange on the high-priority stream,
-    interior bands concurrently on the engine stream (the multi-GPU schedule)."""
+    interior bands concurrently on the engine stream (the multi-GPU schedule).
+    transport=nccl: the halo rows and the check scalars go through the
+    ncclSend / ncclRecv / ncclAllReduce calls of the multi-GPU ranks, posted
+    to a one-rank communicator (NCCL loopback on one GPU)."""
+    from paper_1712_10279_b200 import distributed as D
     from paper_1712_10279_b200.solver import run_local
+    loop = D.SlabCommunicator(pk.solver.nccl_unique_id(), 1, 0, 0) if transport == "nccl" else None
     monkeypatch.setenv("OTFX_OVERLAP", overlap)
     if force_tma:
         monkeypatch.setenv("OTFX_TMA", "1")
@@ -649,7 +656,8 @@ def test_local_slab_run_loop_matches_single_engine(monkeypatch, P, n, force_tma,
         e.set_marginals(l0[bounds[r]:bounds[r + 1]], l1[bounds[r]:bounds[r + 1]])
         slabs.append(e)
     # run_local combines the slabs' own-row ||diff|| itself (no override)
-    hist2, it2, c2 = run_local(slabs, cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+    hist2, it2, c2 = run_local(slabs, cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every,
+                               loopback=loop)
     assert it1 == it2 and c1 == c2 == conv
     g.hist_close(g.hist_array(pk.SolveReport(c1, it1, 0.0, hist1)),
                  g.hist_array(pk.SolveReport(c2, it2, 0.0, hist2)), 1e-12)
@@ -659,6 +667,8 @@ def test_local_slab_run_loop_matches_single_engine(monkeypatch, P, n, force_tma,
         assert np.array_equal(cat, ref_arr), q
     for e in reversed(slabs):
         e.close()
+    if loop is not None:
+        loop.close()
 
 
 # ---------------------------------------------------------------------------
