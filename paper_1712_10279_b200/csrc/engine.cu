@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <chrono>
 #include <cmath>
@@ -42,6 +43,16 @@ struct Error : std::runtime_error {
       throw Error(e_ == cudaErrorMemoryAllocation ? OTFX_ENOMEM : OTFX_ECUDA,                 \
                   std::string(#call) + ": " + cudaGetErrorString(e_));                        \
   } while (0)
+
+// NVTX ranges (header-only NVTX 3: free unless a profiler attaches) around the
+// host-side phases of a solve, so an nsys / ncu timeline shows the run loop,
+// the check periods, the halo exchanges and the host <-> device conversions
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+  Range(const Range&) = delete;
+  Range& operator=(const Range&) = delete;
+};
 
 static void require(bool ok, int code, const std::string& msg) {
   if (!ok) throw Error(code, msg);
@@ -471,7 +482,7 @@ static bool plan_stages(otfx_engine* e, int S) {
   // the consumers hold stages q and q+1, so 2 is the minimum ring; only the
   // 6-warp heavy payloads use it (their stage is released before the W half
   // of the row, whose eigensolves cover the next load)
-  require(S >= (L.cw == 6 ? 2 : 3) && S <= 8, OTFX_EINVAL, "TMA ring depth out of range");
+  require(S >= 2 && S <= 8, OTFX_EINVAL, "TMA ring depth out of range");
   L.tile = 31 * L.cw;  // a multiple of 16 bytes' worth of columns for fp32 and fp64
   L.h = 16 / e->elem;
   L.tw = L.tile + 2 * L.h;
@@ -610,6 +621,7 @@ static void halo_unpack(const otfx_engine* e, bool has_prev, bool has_next, cuda
 
 static void exchange_nccl(otfx_engine* e, cudaStream_t st) {
   if (!e->comm || e->nranks == 1) return;
+  Range nv("otfx.halo_exchange_nccl");
   NcclApi& N = nccl();
   const bool has_prev = e->rank > 0, has_next = e->rank + 1 < e->nranks;
   const size_t w = size_t(e->d.n);
@@ -708,6 +720,7 @@ static void timing_end(otfx_engine* e, int slot, int64_t count) {
 
 static void run_plain(otfx_engine* e, int64_t count) {
   if (count <= 0) return;
+  Range nv("otfx.plain_iterations");
   // NCCL halo exchanges stay outside graph capture unless explicitly enabled
   const bool graphs = e->use_graphs && (e->nranks == 1 || env_int("OTFX_NCCL_GRAPHS", 0) != 0);
   if (!graphs || count < 3) {
@@ -1137,6 +1150,7 @@ static void par_copy(void* dst, const void* src, size_t bytes) {
 // summed block partials {mass0, mass1, weighted sumsq}
 static void host_to_planes(otfx_engine* e, const double* h0, const double* h1, const PackMap& m,
                            void* planes, double sums[3]) {
+  Range nv("otfx.upload");
   PinnedPool& P = pinned_pool();
   std::lock_guard<std::mutex> lock(P.mu);
   cudaEvent_t ev[2] = {P.ev_of(e->d.device)[0], P.ev_of(e->d.device)[1]};
@@ -1183,6 +1197,7 @@ static void host_to_planes(otfx_engine* e, const double* h0, const double* h1, c
 }
 
 static void planes_to_host(otfx_engine* e, const void* planes, const UnpackMap& m, double* h) {
+  Range nv("otfx.download");
   PinnedPool& P = pinned_pool();
   std::lock_guard<std::mutex> lock(P.mu);
   cudaEvent_t ev[2] = {P.ev_of(e->d.device)[0], P.ev_of(e->d.device)[1]};
@@ -1290,6 +1305,7 @@ static void drop_graphs(otfx_engine* e) {
 
 
 static void create(const otfx_engine_desc* d, otfx_engine* e) {
+  Range nv("otfx.create");
   require(d != nullptr, OTFX_EINVAL, "null descriptor");
   e->d = *d;
   const int kind = d->kind;
@@ -1403,7 +1419,9 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     // 96 % at 4 stages vs 92 % at 3)
     // (2 stages are a candidate only for the 6-warp heavy payloads)
     const int wide = e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw;
-    const int smin = (wide == 6 && env_int("OTFX_TMA_WARPS", wide) == wide) ? 2 : 3;
+    // (and for payloads whose 3-stage ring does not fit shared memory)
+    int smin = (wide == 6 && env_int("OTFX_TMA_WARPS", wide) == wide) ? 2 : 3;
+    if (smin == 3 && !plan_stages(e, 3)) smin = 2;
     int S = env_int("OTFX_STAGES", 0);
     if (S <= 0) {
       CK(e->ops64 ? e->ops64->prepare() : e->ops32->prepare());
@@ -1612,6 +1630,7 @@ struct SlabGroup {
 // receive buffer (what ncclSend/ncclRecv move between ranks)
 static void exchange_local_impl(otfx_engine* const* es, int count, cudaStream_t st,
                                 ncclComm_t loop = nullptr) {
+  Range nv("otfx.halo_exchange_local");
   for (int s = 0; s + 1 < count; ++s) {
     otfx_engine* a = es[s];
     otfx_engine* b = es[s + 1];
@@ -1681,6 +1700,7 @@ static void group_plain(const SlabGroup& g, int64_t count) {
 // raw check scalars of the group: NCCL-allreduced for a rank, summed / maxed
 // over the slabs (in slab order) for a local group
 static void group_raw(const SlabGroup& g, bool fused, bool with_res, double raw[OTFX_NRAW]) {
+  Range nv("otfx.check_reduce");
   for (int q = 0; q < OTFX_NRAW; ++q) raw[q] = 0.0;
   for (int s = 0; s < g.count; ++s) {
     otfx_engine* e = g.es[s];
@@ -1705,6 +1725,7 @@ static void copy_history(const otfx_engine* e, otfx_history_point* hist, int64_t
 
 static void run_loop(const SlabGroup& g, const otfx_run_config* cfg, otfx_history_point* hist,
                      int64_t capacity, int64_t* n_history, int64_t* iterations, int* converged) {
+  Range nv("otfx.run");
   otfx_engine* e = g.lead();
   // ||diff|| of the whole grid: the engine's (allreduced under NCCL), or for a
   // local slab group the root of the slabs' summed squares, combined here

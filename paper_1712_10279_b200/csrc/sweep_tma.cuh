@@ -171,7 +171,9 @@ template <class P, typename T, int FL, int CWT = 4>
 // The 4-warp instantiations (matrix payloads) keep ptxas' default (0 = no
 // hint): stating minBlocks = 1 there raises the 3x3 real payload from 156 to
 // 196 registers and halves its occupancy.
-__global__ void __launch_bounds__(32 * (CWT + 1), CWT == 8 ? (FL != 0 ? 2 : 1) : 0) sweep_tma_kernel(
+__global__ void __launch_bounds__(32 * (CWT + 1),
+                                  (CWT == 8 && (P::NCOEF > 0 || !P::HAS_W)) ? (FL != 0 ? 2 : 1) : 0)
+    sweep_tma_kernel(
     const __grid_constant__ TmaSweepArgs<T> G, const __grid_constant__ TmaSet M) {
   constexpr bool CHECK = (FL & 1) != 0;
   constexpr bool DUAL = (FL & 2) != 0;
