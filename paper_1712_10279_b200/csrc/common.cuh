@@ -73,6 +73,10 @@ struct SweepArgs {
   double* maxes;         // evaluate: [blocks][2]
   double* dualp;         // DUAL sweeps: [blocks][4] = PENU, PENW, GU, GW
   double coef[MAX_CHAN_COEF];  // graph D/c (k x ell, row-major) or Lindblad (ell,k,k,{re,im})
+  // runtime-size payloads (dyn.cuh): channel count and the graph D/c in
+  // device memory (k x ell, row-major); unused by the compiled policies
+  int nchan;
+  const double* chan_dev;
 };
 
 template <typename T>

@@ -138,7 +138,7 @@ struct PackMap {
   int src[MAXMAP];        // record index per plane (-1: zero)
   double wt[MAXMAP];      // plane weight for the sum of squares
   int nmass;              // record indices summed into the mass
-  int mass[16];
+  int mass[64];            // (up to DYN_KMAX channels)
 };
 
 struct UnpackMap {
@@ -344,6 +344,9 @@ struct otfx_engine {
   // policy dispatch
   const otfx::Ops<double>* ops64 = nullptr;
   const otfx::Ops<float>* ops32 = nullptr;
+  // the channel operator in device memory (runtime-size payloads, dyn.cuh)
+  double* d_chan = nullptr;
+  bool dynamic() const { return ops64 ? ops64->dynamic : (ops32 && ops32->dynamic); }
 };
 
 namespace otfx {
@@ -386,7 +389,11 @@ static SweepArgs<T> make_args(otfx_engine* e, int from) {
   a.maxes = nullptr;
   a.dualp = e->d_part_dual;
   const int K = e->K;
-  if (e->d.kind == OTFX_KIND_VECTOR) {
+  a.nchan = K;
+  a.chan_dev = e->d_chan;
+  if (e->dynamic()) {
+    // the kernels read the graph from d_chan
+  } else if (e->d.kind == OTFX_KIND_VECTOR) {
     const int L = e->LMAX;
     for (int c = 0; c < K; ++c)
       for (int q = 0; q < e->d.ell; ++q) a.coef[c * L + q] = e->chan[size_t(c) * e->d.ell + q];
@@ -905,7 +912,7 @@ static void finalize(const otfx_engine* e, const double* raw, double out[5], dou
 
 // ---- maps -----------------------------------------------------------------
 static void add_mass(PackMap& m, int idx) {
-  require(m.nmass < 16, OTFX_EUNSUPPORTED, "mass map overflow");
+  require(m.nmass < 64, OTFX_EUNSUPPORTED, "mass map overflow");
   m.mass[m.nmass++] = idx;
 }
 
@@ -1338,7 +1345,8 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     require(d->nu > 0 && d->alpha > 0, OTFX_EINVAL, "nu and alpha must be positive");
     require(d->chan != nullptr, OTFX_EINVAL, "channel operator missing");
     const size_t nc = kind == OTFX_KIND_VECTOR ? size_t(e->K) * d->ell : size_t(d->ell) * e->K * e->K * 2;
-    require(nc <= size_t(MAX_CHAN_COEF), OTFX_EUNSUPPORTED, "channel operator too large");
+    require(e->dynamic() || nc <= size_t(MAX_CHAN_COEF), OTFX_EUNSUPPORTED,
+            "channel operator too large");
     e->chan.assign(d->chan, d->chan + nc);
     e->NWact = d->ell * NWS;
   } else {
@@ -1410,7 +1418,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   // TMA-streamed sweep: ring depth 4 (3 if that keeps two CTAs per SM)
   // the TMA ring pays off once rows are long enough to pipeline; small slabs
   // run the register-streamed sweep (measured: 4.4 vs 8.9 us/iteration at 64^2)
-  e->use_tma = env_int("OTFX_TMA", small ? 0 : 1) != 0;
+  e->use_tma = env_int("OTFX_TMA", small ? 0 : 1) != 0 && !e->dynamic();
   if (e->use_tma) {
     // ring depth: 3 or 4 stages, whichever keeps more CTAs resident per SM
     // (registers and shared memory both count); on a tie the deeper ring
@@ -1500,7 +1508,9 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   }
 
   // staging: up to 64 MB, at least two grid rows of the widest record
-  const int max_rec = std::max(2 * e->K * e->K * std::max(1, d->ell) * 2, 16);
+  const int max_rec = (kind == OTFX_KIND_VECTOR || kind == OTFX_KIND_SCALAR)
+                          ? std::max(std::max(2 * e->K, int(d->ell)), 16)
+                          : std::max(2 * e->K * e->K * std::max(1, d->ell) * 2, 16);
   e->stage_bytes = std::max<size_t>(size_t(128) << 20, size_t(4) * n * max_rec * sizeof(double));
 
   const size_t n_sweep = size_t(e->gx) * e->gy * 10, n_pe = size_t(e->ex) * e->ey * 8,
@@ -1520,6 +1530,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   const size_t o_pack = carve(kPackBlocks * 3 * 8);
   const size_t o_halo = carve(halo);
   const size_t o_result = carve(4 * sizeof(long long));
+  const size_t o_chan = carve(e->chan.size() * sizeof(double));
   const size_t o_stage = carve(e->stage_bytes);
   e->total_bytes = off;
   // stream-ordered allocation from the library's per-device pool: freed
@@ -1549,6 +1560,11 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   e->d_pack_part = reinterpret_cast<double*>(e->mem + o_pack);
   e->d_halo = e->mem + o_halo;
   e->d_result = reinterpret_cast<long long*>(e->mem + o_result);
+  if (e->dynamic()) {
+    e->d_chan = reinterpret_cast<double*>(e->mem + o_chan);
+    CK(cudaMemcpyAsync(e->d_chan, e->chan.data(), e->chan.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, e->stream));
+  }
   e->d_stage = reinterpret_cast<double*>(e->mem + o_stage);
   if (e->use_tma) {
     for (int st = 0; st < 2; ++st) {

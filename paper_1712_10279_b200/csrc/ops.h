@@ -38,11 +38,16 @@ struct Ops {
                              cudaStream_t s);
   size_t (*cluster_smem)(int rows_max, int n);
   int (*cluster_fits)(int ctas, int threads, size_t smem);  // 1 if such a cluster can launch
+  // runtime-size payload (dyn.cuh): k and the graph D/c come from the kernel
+  // arguments (nchan, chan_dev), no TMA sweep
+  bool dynamic = false;
 };
 
 // registries, one per instantiation unit
 const Ops<double>* ops_vector_f64(int K, bool has_w);
 const Ops<float>* ops_vector_f32(int K, bool has_w);
+const Ops<double>* ops_vector_dyn_f64(int K);  // k beyond the compiled policies
+const Ops<float>* ops_vector_dyn_f32(int K);
 const Ops<double>* ops_matrix_f64(int kind, int K, int ell);
 const Ops<float>* ops_matrix_f32(int kind, int K, int ell);
 

@@ -8,7 +8,8 @@ const Ops<float>* ops_vector_f32_wide(int K);
 
 const Ops<float>* ops_vector_f32(int K, bool has_w) {
   if (!has_w || K <= 3) return ops_vector_f32_small(K, has_w);
-  return ops_vector_f32_wide(K);
+  const Ops<float>* o = ops_vector_f32_wide(K);
+  return o ? o : ops_vector_dyn_f32(K);
 }
 
 }  // namespace otfx

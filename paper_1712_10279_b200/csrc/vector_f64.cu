@@ -8,7 +8,8 @@ const Ops<double>* ops_vector_f64_wide(int K);
 
 const Ops<double>* ops_vector_f64(int K, bool has_w) {
   if (!has_w || K <= 3) return ops_vector_f64_small(K, has_w);
-  return ops_vector_f64_wide(K);
+  const Ops<double>* o = ops_vector_f64_wide(K);
+  return o ? o : ops_vector_dyn_f64(K);
 }
 
 }  // namespace otfx

@@ -2,10 +2,12 @@
 TransportGraph (S/graph.py:23-70) takes any connected graph on k nodes and its
 LindbladSet (S/lindblad.py:47-66) any ell Hermitian k x k matrices with a
 nondegenerate gradient.  The engine instantiates vector payloads for
-k = 2..8 and matrix payloads for k = 2..4 with ell <= 4, and k = 2, 3 with
-ell <= 8 (the eight Gell-Mann matrices of su(3)); each is checked here against
-the oracle through every execution path, and what lies outside is rejected
-with UnsupportedNormError before any device work."""
+k = 2..8 (compiled, state in registers) and runs k = 9..32 (up to 128 edges)
+on the runtime-size payload (csrc/dyn.cuh); matrix payloads are compiled for
+k = 2..4 with ell <= 4, and k = 2, 3 with ell <= 8 (the eight Gell-Mann
+matrices of su(3)).  Each is checked here against the oracle through every
+execution path, and what lies outside is rejected with UnsupportedNormError
+before any device work."""
 
 import numpy as np
 import pytest
@@ -118,10 +120,83 @@ def test_matrix_lindblad_counts(monkeypatch, path, case):
     _check(rep, st, eng, iters, ce, bit_exact=False)
 
 
+@pytest.mark.parametrize("path", ["default", "tma"])
+@pytest.mark.parametrize("k,graph_kind,norms,eps", [
+    (9, "chain", ("l12", "l1"), 0.0), (12, "complete", ("l2", "l2"), 0.0),
+    (16, "complete", ("l12", "l1"), 0.0), (10, "star", ("l1", "l1"), 0.01),
+    (24, "chain", ("l2", "l1"), 0.0),
+])
+def test_vector_runtime_width(monkeypatch, path, k, graph_kind, norms, eps):
+    """Graphs wider than the compiled policies (k > 8) run on the runtime-size
+    payload (csrc/dyn.cuh): same operation order as the compiled vector path,
+    so the iterates EQUAL the oracle's (which is pinned to the reference)."""
+    for key, val in PATHS[path].items():
+        monkeypatch.setenv(key, val)
+    rng = np.random.default_rng(k * 7 + len(graph_kind))
+    if graph_kind == "chain":
+        edges = [(c, c + 1) for c in range(k - 1)]
+    elif graph_kind == "star":
+        edges = [(0, c) for c in range(1, k)]
+    else:
+        edges = [(a, b) for a in range(k) for b in range(a + 1, k)]
+    graph = pk.TransportGraph(k, edges, rng.uniform(0.5, 2.0, len(edges)))
+    n, iters, ce, tau, alpha = 36, 50, 25, 3.0, 0.05
+    l0, l1 = _norm(rng, (n, n, k)), _norm(rng, (n, n, k))
+    cfg = pk.SolverConfig(tau=tau, norm_u=norms[0], norm_w=norms[1], alpha=alpha, eps_reg=eps,
+                          tol_gap=1e-300, tol_feas=1e-300, max_iters=iters, check_every=ce)
+    rep, st = pk.solve_vector(pk.VectorDensity(l0), pk.VectorDensity(l1), graph, cfg=cfg)
+    eng = pdhg.OracleEngine("vector", l0 - l1, n, tau, norm_u=norms[0], norm_w=norms[1],
+                            alpha=alpha, eps=eps, chan=graph.coefficients(),
+                            lam_chan=pk.lambda_max_graph(graph))
+    _check(rep, st, eng, iters, ce, bit_exact=True)
+    if k == 9:
+        assert np.count_nonzero(st.w.values) > 0  # the channel flux is active
+
+
+def test_runtime_width_slabs_match_one_engine():
+    """The runtime-size payload under the multi-slab run loop (overlapped
+    halo exchange, NCCL loopback transport): the slabs' state equals one
+    engine's."""
+    from paper_1712_10279_b200 import distributed as D
+    from paper_1712_10279_b200.solver import build_engine, run_local
+
+    rng = np.random.default_rng(5)
+    k, n = 11, 96
+    graph = pk.TransportGraph(k, [(c, c + 1) for c in range(k - 1)] + [(0, k - 1)],
+                              rng.uniform(0.5, 2.0, k))
+    l0, l1 = _norm(rng, (n, n, k)), _norm(rng, (n, n, k))
+    cfg = pk.SolverConfig(tau=3.0, norm_u="l12", norm_w="l1", alpha=0.05, tol_gap=1e-300,
+                          tol_feas=1e-300, max_iters=60, check_every=20)
+    whole = build_engine("vector", n, cfg, graph=graph)
+    whole.set_marginals(l0, l1)
+    hist1, it1, _, _ = whole.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+    ref = whole.get_state()
+    whole.close()
+    loop = D.SlabCommunicator(pk.solver.nccl_unique_id(), 1, 0, 0)
+    bounds, slabs, stream = [0, 40, n], [], None
+    for r in range(2):
+        e = build_engine("vector", n, cfg, graph=graph, rows=(bounds[r], bounds[r + 1]),
+                         stream=stream)
+        stream = e.stream
+        e.set_marginals(l0[bounds[r]:bounds[r + 1]], l1[bounds[r]:bounds[r + 1]])
+        slabs.append(e)
+    hist2, it2, _ = run_local(slabs, cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every,
+                              loopback=loop)
+    assert it1 == it2
+    g.hist_close(g.hist_array(pk.SolveReport(False, it1, 0.0, hist1)),
+                 g.hist_array(pk.SolveReport(False, it2, 0.0, hist2)), 1e-12)
+    got = [e.get_state() for e in slabs]
+    for q, want in enumerate(ref):
+        assert np.array_equal(np.concatenate([s[q] for s in got], axis=0), want), q
+    for e in reversed(slabs):
+        e.close()
+    loop.close()
+
+
 def test_outside_the_instantiations_is_rejected():
     rng = np.random.default_rng(0)
     n = 8
-    k = 9
+    k = 33  # beyond the runtime-size payload's 32 channels
     graph = pk.TransportGraph(k, [(c, c + 1) for c in range(k - 1)], np.ones(k - 1))
     l0, l1 = _norm(rng, (n, n, k)), _norm(rng, (n, n, k))
     with pytest.raises(pk.UnsupportedNormError):
