@@ -58,6 +58,10 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-secondary", action="store_true",
                    help="skip the BASELINE configs[0..3] side measurements")
+    p.add_argument("--dist", action="store_true",
+                   help="take the multi-rank code path (process group, NCCL id broadcast, "
+                        "slab communicator, solve_vector_rows) even at world size 1, under "
+                        "torchrun: the one-GPU check of what an N-GPU run executes")
     return p.parse_args()
 
 
@@ -277,7 +281,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    multi = world > 1 or args.dist
+    if multi:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = global_n(args.n, world)
     b = D.slab_bounds(n, world)
@@ -288,7 +293,7 @@ def run_ours(args):
     graph = pk.triangle_graph()
     l0, l1 = synthetic.rgb_disk_rows(n, r0, r1)
     stream = torch.cuda.Stream()
-    uid = D.share_unique_id(dist, rank) if world > 1 else None
+    uid = D.share_unique_id(dist, rank) if multi else None
     eng = D.make_vector_slab_engine(n, graph, cfg, nranks=world, rank=rank, unique_id=uid,
                                     precision=args.precision, device=local,
                                     stream=stream.cuda_stream)
@@ -298,7 +303,7 @@ def run_ours(args):
     # warm-up: W check periods through the run loop (graph capture, clocks)
     eng.run(1e-300, 1e-300, args.warmup * ips, ips)
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     eng.timing(1)
@@ -318,7 +323,7 @@ def run_ours(args):
     if not sweep_ms > 0:  # no plain iterations timed: fall back to the whole step
         sweep_ms = ms / max(args.steps * ips, 1)
     t = torch.tensor([ms, sweep_ms], device="cuda")
-    if world > 1:
+    if multi:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, sweep_ms = float(t[0]), float(t[1])
     cells = float(n) * n
@@ -340,7 +345,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(args, n, r0, r1, world, rank, local, uid_fn=lambda: (
-            D.share_unique_id(dist, rank) if world > 1 else None))
+            D.share_unique_id(dist, rank) if multi else None), multi=multi)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.ref_n, args.cpu_seconds)
@@ -391,7 +396,7 @@ def run_ours(args):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -571,7 +576,7 @@ def north_star_4096(args, device):
     return out
 
 
-def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn):
+def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn, multi=False):
     """End to end through the public API: host marginals in, host state out."""
     import torch
 
@@ -584,7 +589,7 @@ def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn):
                           tol_feas=1e-300, max_iters=M, check_every=100)
     graph = pk.triangle_graph()
     l0, l1 = synthetic.rgb_disk_rows(n, r0, r1)
-    if world == 1:
+    if not multi:
         a, b = pk.VectorDensity(l0), pk.VectorDensity(l1)
 
         def call():
@@ -600,20 +605,20 @@ def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn):
     call()  # warm-up (allocations, graph capture)
     times = []
     for _ in range(args.e2e_steps):
-        if world > 1:
+        if multi:
             torch.distributed.barrier()
         t0 = time.perf_counter()
         rep, st = call()
         times.append(time.perf_counter() - t0)
     t = torch.tensor([float(np.mean(times))], device="cuda")
-    if world > 1:
+    if multi:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         comm.close()  # every rank, same point
     sec = float(t[0])
     cells = float(n) * n
     rows_cells = float(r1 - r0) * n
     breakdown = None
-    if world == 1:
+    if not multi:
         # one instrumented solve through the engine API (not part of the timed steps)
         from paper_1712_10279_b200.solver import build_engine
 
@@ -636,7 +641,7 @@ def measure_e2e(args, n, r0, r1, world, rank, local, uid_fn):
             "h2d_bytes_per_step": int(2 * rows_cells * K_CH * 8),
             "d2h_bytes_per_step": int(rows_cells * (2 * K_CH + ELL + K_CH) * 8),
             "iterations_per_step": M, "seconds_per_step": sec,
-            "api": "paper_1712_10279_b200.solve_vector (host numpy in/out)" if world == 1 else
+            "api": "paper_1712_10279_b200.solve_vector (host numpy in/out)" if not multi else
                    "paper_1712_10279_b200.distributed.solve_vector_rows"}
 
 

@@ -67,13 +67,15 @@ template <>
 const Ops<double>* find_ops<double>(int kind, int K, int ell) {
   if (kind == KIND_SCALAR) return ops_vector_f64(1, false);
   if (kind == KIND_VECTOR) return ops_vector_f64(K, true);
-  return ops_matrix_f64(kind, K, ell);
+  const Ops<double>* o = ops_matrix_f64(kind, K, ell);
+  return o ? o : ops_matrix_dyn_f64(kind, K);
 }
 template <>
 const Ops<float>* find_ops<float>(int kind, int K, int ell) {
   if (kind == KIND_SCALAR) return ops_vector_f32(1, false);
   if (kind == KIND_VECTOR) return ops_vector_f32(K, true);
-  return ops_matrix_f32(kind, K, ell);
+  const Ops<float>* o = ops_matrix_f32(kind, K, ell);
+  return o ? o : ops_matrix_dyn_f32(kind, K);
 }
 
 // ---------------------------------------------------------------------------
@@ -130,7 +132,9 @@ static NcclApi& nccl() {
 // ---------------------------------------------------------------------------
 // layout conversion kernels (reference AoS <-> device planes)
 // ---------------------------------------------------------------------------
-constexpr int MAXMAP = 256;
+// record reals of one cell: up to the runtime-size matrix payload's w record
+// (real path ell * k^2 <= 1024 at k = 2, complex 2 * ell * k^2 <= 512)
+constexpr int MAXMAP = 1024;
 
 struct PackMap {
   int np;                 // planes written
@@ -1032,6 +1036,7 @@ static PackMap flux_w_pack(const otfx_engine* e) {
   // engine holds it (S/solver.py:414-432); complex path: complex128
   const int cs = e->d.kind == OTFX_KIND_MATRIX_REAL ? 1 : 2;
   m.rec = cs * ell * K * K;
+  require(m.rec <= MAXMAP && m.np <= MAXMAP, OTFX_EUNSUPPORTED, "channel flux record too large");
   const int NWS = e->NWS;
   for (int s = 0; s < ell; ++s) {
     const int base = cs * s * K * K;
@@ -1074,6 +1079,7 @@ static UnpackMap flux_w_unpack(const otfx_engine* e) {
   }
   const int cs = e->d.kind == OTFX_KIND_MATRIX_REAL ? 1 : 2;
   m.rec = cs * ell * K * K;
+  require(m.rec <= MAXMAP, OTFX_EUNSUPPORTED, "channel flux record too large");
   const int NWS = e->NWS;
   for (int s = 0; s < ell; ++s) {
     const int base = cs * s * K * K;

@@ -48,6 +48,8 @@ const Ops<double>* ops_vector_f64(int K, bool has_w);
 const Ops<float>* ops_vector_f32(int K, bool has_w);
 const Ops<double>* ops_vector_dyn_f64(int K);  // k beyond the compiled policies
 const Ops<float>* ops_vector_dyn_f32(int K);
+const Ops<double>* ops_matrix_dyn_f64(int kind, int K);  // (k, ell) beyond the compiled ones
+const Ops<float>* ops_matrix_dyn_f32(int kind, int K);
 const Ops<double>* ops_matrix_f64(int kind, int K, int ell);
 const Ops<float>* ops_matrix_f32(int kind, int K, int ell);
 

@@ -5,7 +5,8 @@ nondegenerate gradient.  The engine instantiates vector payloads for
 k = 2..8 (compiled, state in registers) and runs k = 9..32 (up to 128 edges)
 on the runtime-size payload (csrc/dyn.cuh); matrix payloads are compiled for
 k = 2..4 with ell <= 4, and k = 2, 3 with ell <= 8 (the eight Gell-Mann
-matrices of su(3)).  Each is checked here against the oracle through every
+matrices of su(3)), and run on the runtime-size matrix payload beyond that
+(k <= 8, ell * block reals <= 256: su(4)'s 15 generators at k = 4).  Each is checked here against the oracle through every
 execution path, and what lies outside is rejected with UnsupportedNormError
 before any device work."""
 
@@ -153,6 +154,42 @@ def test_vector_runtime_width(monkeypatch, path, k, graph_kind, norms, eps):
         assert np.count_nonzero(st.w.values) > 0  # the channel flux is active
 
 
+@pytest.mark.parametrize("path", ["default", "tma"])
+@pytest.mark.parametrize("k,ell,cplx,norms", [
+    (4, 6, True, ("l1nuc", "l1nuc")), (4, 15, True, ("l2", "l1")), (5, 3, False, ("l2", "l1")),
+    (5, 2, True, ("l1nuc", "l1nuc")), (6, 3, True, ("l1", "l2")), (2, 10, False, ("l12", "l1")),
+])
+def test_matrix_runtime_size(monkeypatch, path, k, ell, cplx, norms):
+    """Matrix payloads beyond the compiled (k, ell) instantiations run on the
+    runtime-size payload (csrc/dyn.cuh DynMat): packed layouts, commutators
+    and the Jacobi eigen-shrink of the compiled policies with runtime k;
+    held to the north star's 1e-10 against the oracle (which runs LAPACK)."""
+    for key, val in PATHS[path].items():
+        monkeypatch.setenv(key, val)
+    rng = np.random.default_rng(k * 100 + ell)
+    n, iters, ce, tau, alpha = 16, 30, 15, 10.0, 0.3
+    a = rng.normal(size=(ell, k, k))
+    if cplx:
+        a = a + 1j * rng.normal(size=(ell, k, k))
+        mats = 0.5 * (a + np.conj(np.swapaxes(a, -1, -2)))
+    else:
+        mats = 0.5 * (a + np.swapaxes(a, -1, -2))
+    lind = pk.LindbladSet(mats.astype(np.complex128))
+    l0, l1 = _psd(rng, n, k, cplx), _psd(rng, n, k, cplx)
+    cfg = pk.SolverConfig(tau=tau, norm_u=norms[0], norm_w=norms[1], alpha=alpha,
+                          tol_gap=1e-300, tol_feas=1e-300, max_iters=iters, check_every=ce)
+    rep, st = pk.solve_matrix(pk.MatrixDensity(l0), pk.MatrixDensity(l1), lind, cfg=cfg)
+    real_path = st.phi.dtype == np.float64
+    assert real_path == (not cplx)
+    dt = np.float64 if real_path else np.complex128
+    diff = (l0 - l1).real if real_path else (l0 - l1)
+    chan = lind.matrices.real if real_path else lind.matrices
+    eng = pdhg.OracleEngine("matrix", diff.astype(dt), n, tau, norm_u=norms[0], norm_w=norms[1],
+                            alpha=alpha, chan=chan, lam_chan=pk.lambda_max_L(lind), dtype=dt)
+    _check(rep, st, eng, iters, ce, bit_exact=False)
+    assert np.count_nonzero(st.w.values) > 0
+
+
 def test_runtime_width_slabs_match_one_engine():
     """The runtime-size payload under the multi-slab run loop (overlapped
     halo exchange, NCCL loopback transport): the slabs' state equals one
@@ -195,6 +232,14 @@ def test_runtime_width_slabs_match_one_engine():
 
 def test_outside_the_instantiations_is_rejected():
     rng = np.random.default_rng(0)
+    # a 9x9 matrix payload is beyond the runtime-size matrix capacity (8)
+    k9 = 9
+    lind = pk.LindbladSet(np.stack([np.diag(np.arange(k9, dtype=float)),
+                                    np.eye(k9, k=1) + np.eye(k9, k=-1)]).astype(np.complex128))
+    m0, m1 = _psd(rng, 6, k9, False), _psd(rng, 6, k9, False)
+    with pytest.raises(pk.UnsupportedNormError):
+        pk.solve_matrix(pk.MatrixDensity(m0), pk.MatrixDensity(m1), lind,
+                        cfg=pk.SolverConfig(max_iters=10))
     n = 8
     k = 33  # beyond the runtime-size payload's 32 channels
     graph = pk.TransportGraph(k, [(c, c + 1) for c in range(k - 1)], np.ones(k - 1))
