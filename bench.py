@@ -45,7 +45,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--precision", choices=["f64", "f32"], default="f64")
-    p.add_argument("--n", type=int, default=8192, help="grid side per GPU (weak scaling)")
+    p.add_argument("--n", "--side", type=int, default=8192,
+                   help="grid side per GPU (weak scaling)")
     p.add_argument("--iters-per-step", type=int, default=100)
     # one e2e call = a 2000-iteration solve, the fixed count of BASELINE configs[0]
     p.add_argument("--e2e-iters", type=int, default=2000)

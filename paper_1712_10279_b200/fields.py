@@ -65,6 +65,26 @@ def _grid_array(values, min_ndim, who):
 
 
 class _Density:
+    """An (n, n, payload) marginal, validated on construction.  The three
+    kinds differ in rank, dtype and a per-kind check (`_admit`); the error
+    classes and messages are the reference's."""
+
+    _RANK = 2
+    _DTYPE = np.float64
+
+    def __post_init__(self):
+        who = type(self).__name__
+        arr = _grid_array(self.values, self._RANK, who).astype(self._DTYPE)
+        object.__setattr__(self, "values", self._admit(arr, who))
+
+    @classmethod
+    def _admit(cls, arr, who):
+        if arr.ndim != cls._RANK:
+            raise ValidationError(f"{who}: expected {cls._RANK}-d array, got {arr.ndim}-d")
+        if arr.min() < 0:
+            raise ValidationError(f"{who}: negative entries")
+        return arr
+
     @property
     def n(self) -> int:
         return self.values.shape[0]
@@ -73,56 +93,43 @@ class _Density:
     def grid(self) -> GridSpec:
         return GridSpec(self.n)
 
+    @property
+    def k(self) -> int:
+        """channels (vector) or matrix side (matrix) of the payload"""
+        return self.values.shape[2]
+
 
 @dataclass(frozen=True)
 class ScalarDensity(_Density):
     values: np.ndarray
 
-    def __post_init__(self):
-        arr = _grid_array(self.values, 2, "ScalarDensity").astype(np.float64)
-        if arr.ndim != 2:
-            raise ValidationError(f"ScalarDensity: expected 2-d array, got {arr.ndim}-d")
-        if arr.min() < 0:
-            raise ValidationError("ScalarDensity: negative entries")
-        object.__setattr__(self, "values", arr)
-
 
 @dataclass(frozen=True)
 class VectorDensity(_Density):
     values: np.ndarray
-
-    def __post_init__(self):
-        arr = _grid_array(self.values, 3, "VectorDensity").astype(np.float64)
-        if arr.ndim != 3:
-            raise ValidationError(f"VectorDensity: expected 3-d array, got {arr.ndim}-d")
-        if arr.min() < 0:
-            raise ValidationError("VectorDensity: negative entries")
-        object.__setattr__(self, "values", arr)
-
-    @property
-    def k(self) -> int:
-        return self.values.shape[2]
+    _RANK = 3
 
 
 @dataclass(frozen=True)
 class MatrixDensity(_Density):
-    values: np.ndarray
+    """Per-cell Hermitian PSD k x k matrices; stored as their exact
+    Hermitian part."""
 
-    def __post_init__(self):
-        arr = _grid_array(self.values, 4, "MatrixDensity").astype(np.complex128)
+    values: np.ndarray
+    _RANK = 4
+    _DTYPE = np.complex128
+
+    @classmethod
+    def _admit(cls, arr, who):
         if arr.ndim != 4 or arr.shape[2] != arr.shape[3]:
-            raise ValidationError(f"MatrixDensity: expected (n, n, k, k), got {arr.shape}")
+            raise ValidationError(f"{who}: expected (n, n, k, k), got {arr.shape}")
         scale = max(float(np.max(np.abs(arr))), 1.0)
         if _defect(arr, 1) > 1e-10 * scale:
-            raise ValidationError("MatrixDensity: per-cell matrices not Hermitian")
-        arr = hermitian_part(arr)
-        if float(np.linalg.eigvalsh(arr).min()) < PSD_EIG_TOL * scale:
-            raise ValidationError("MatrixDensity: matrix below the PSD tolerance")
-        object.__setattr__(self, "values", arr)
-
-    @property
-    def k(self) -> int:
-        return self.values.shape[2]
+            raise ValidationError(f"{who}: per-cell matrices not Hermitian")
+        herm = hermitian_part(arr)
+        if float(np.linalg.eigvalsh(herm).min()) < PSD_EIG_TOL * scale:
+            raise ValidationError(f"{who}: matrix below the PSD tolerance")
+        return herm
 
     def trace_field(self) -> np.ndarray:
         return np.real(np.trace(self.values, axis1=2, axis2=3))
@@ -188,21 +195,22 @@ class GraphFlux:
     values: np.ndarray
 
     def __post_init__(self):
-        object.__setattr__(self, "values",
-                           _grid_array(self.values, 3, "GraphFlux").astype(np.float64))
+        arr = _grid_array(self.values, 3, type(self).__name__)
+        object.__setattr__(self, "values", arr.astype(np.float64))
 
 
 @dataclass(frozen=True)
 class QuantumFlux:
-    """Per-cell stacks of ell skew-Hermitian k x k matrices (n, n, ell, k, k)."""
+    """Per-cell stacks of ell skew-Hermitian k x k matrices (n, n, ell, k, k),
+    stored as their exact skew part."""
 
     values: np.ndarray
 
     def __post_init__(self):
-        arr = _grid_array(self.values, 5, "QuantumFlux").astype(np.complex128)
+        who = type(self).__name__
+        arr = _grid_array(self.values, 5, who).astype(np.complex128)
         if arr.ndim != 5 or arr.shape[3] != arr.shape[4]:
-            raise ValidationError(f"QuantumFlux: expected (n, n, ell, k, k), got {arr.shape}")
-        scale = max(float(np.max(np.abs(arr))), 1.0)
-        if _defect(arr, -1) > 1e-10 * scale:
-            raise ValidationError("QuantumFlux: matrices not skew-Hermitian")
+            raise ValidationError(f"{who}: expected (n, n, ell, k, k), got {arr.shape}")
+        if _defect(arr, -1) > 1e-10 * max(float(np.max(np.abs(arr))), 1.0):
+            raise ValidationError(f"{who}: matrices not skew-Hermitian")
         object.__setattr__(self, "values", skew_part(arr))

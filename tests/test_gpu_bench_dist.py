@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_bench_multi_rank_path_world1():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
            "--master-addr", "127.0.0.1", "--master-port", "29537", "bench.py", "--dist",
-           "--n", "1024", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-secondary",
+           "--side", "1024", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-secondary",
            "--e2e-iters", "200", "--e2e-steps", "1"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
