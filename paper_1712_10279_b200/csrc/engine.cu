@@ -350,6 +350,8 @@ struct otfx_engine {
   const otfx::Ops<float>* ops32 = nullptr;
   // the channel operator in device memory (runtime-size payloads, dyn.cuh)
   double* d_chan = nullptr;
+  // device-side run loop (run_loop_device): loop control block
+  void* d_loop = nullptr;
   bool dynamic() const { return ops64 ? ops64->dynamic : (ops32 && ops32->dynamic); }
 };
 
@@ -1537,6 +1539,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   const size_t o_halo = carve(halo);
   const size_t o_result = carve(4 * sizeof(long long));
   const size_t o_chan = carve(e->chan.size() * sizeof(double));
+  const size_t o_loop = carve(256);
   const size_t o_stage = carve(e->stage_bytes);
   e->total_bytes = off;
   // stream-ordered allocation from the library's per-device pool: freed
@@ -1566,6 +1569,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   e->d_pack_part = reinterpret_cast<double*>(e->mem + o_pack);
   e->d_halo = e->mem + o_halo;
   e->d_result = reinterpret_cast<long long*>(e->mem + o_result);
+  e->d_loop = e->mem + o_loop;
   if (e->dynamic()) {
     e->d_chan = reinterpret_cast<double*>(e->mem + o_chan);
     CK(cudaMemcpyAsync(e->d_chan, e->chan.data(), e->chan.size() * sizeof(double),
@@ -1745,6 +1749,125 @@ static void copy_history(const otfx_engine* e, otfx_history_point* hist, int64_t
   *n_history = nh;
 }
 
+// ---- device-side run loop ----------------------------------------------------
+// Small grids spend a host round trip per check (check sweep -> evaluate ->
+// reduce -> copy -> stream sync -> host finalize -> next graph launch): ~40 us
+// per 100 iterations at 256^2, 6-8 % of the run (tools/check_overhead.py).
+// Here the check periods run inside ONE CUDA graph: a WHILE conditional node
+// whose body is a period -- ce - 1 plain sweeps, the check sweep, evaluate,
+// the fixed-order reduction and loop_check_kernel, which applies the
+// reference's finalize algebra (S/solver.py:242-291, finalize_dev), appends the
+// history row on the device, takes the stopping decision (:315-316) and sets
+// the loop condition.  Same kernels and reductions as the host loop, so the
+// iterates and history are identical; the host syncs once per run.
+struct LoopCtl {
+  double tol_gap, tol_feas, diff_norm;
+  long long it, ce, periods_left, nh, hist_cap;
+  int conv;
+};
+
+__global__ void loop_check_kernel(const double* raw, LoopCtl* c, double* hist, double mu, double nu,
+                                  double tau, double alpha, double eps, int has_w,
+                                  cudaGraphConditionalHandle h) {
+  if (threadIdx.x != 0) return;
+  double out[5];
+  finalize_dev(raw, has_w != 0, alpha, eps, c->diff_norm, mu, nu, tau, out);
+  c->it += c->ce;
+  const bool conv = out[2] <= c->tol_gap && out[3] <= c->tol_feas;
+  double* r = hist + c->nh * 6;
+  r[0] = double(c->it);
+  r[1] = out[0];
+  r[2] = out[1];
+  r[3] = out[2];
+  r[4] = out[3];
+  r[5] = out[4];
+  c->nh += 1;
+  c->periods_left -= 1;
+  c->conv = conv ? 1 : 0;
+  cudaGraphSetConditional(h, (!conv && c->periods_left > 0 && c->nh < c->hist_cap) ? 1u : 0u);
+}
+
+static cudaGraphExec_t loop_graph(otfx_engine* e, int64_t ce) {
+  const auto key = std::make_pair(e->cur, -ce);  // plain graphs use positive counts
+  auto it = e->graphs.find(key);
+  if (it != e->graphs.end()) return it->second;
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  const int saved = e->cur;
+  CK(cudaStreamBeginCaptureToGraph(e->stream, body, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal));
+  try {
+    for (int64_t q = 0; q + 1 < ce; ++q) launch_sweep(e, 0);
+    launch_sweep(e, 1);
+    launch_evaluate(e);
+    reduce_raw_kernel<<<1, 256, 0, e->stream>>>(e->d_part_eval, e->d_max_eval, e->ex * e->ey,
+                                                 e->d_part_sweep, e->gx * e->gy, 1, e->d_raw);
+    CK(cudaGetLastError());
+    loop_check_kernel<<<1, 32, 0, e->stream>>>(e->d_raw, static_cast<LoopCtl*>(e->d_loop),
+                                               e->d_stage, e->d.mu, e->d.nu, e->d.tau, e->d.alpha,
+                                               e->d.eps_reg, e->has_w ? 1 : 0, h);
+    CK(cudaGetLastError());
+  } catch (...) {
+    cudaStreamEndCapture(e->stream, &body);
+    e->cur = saved;
+    cudaGraphDestroy(g);
+    throw;
+  }
+  CK(cudaStreamEndCapture(e->stream, &body));
+  e->cur = saved;  // ce is even: the period ends on the iterate parity it started from
+  cudaGraphExec_t ge;
+  CK(cudaGraphInstantiate(&ge, g, 0));
+  cudaGraphDestroy(g);
+  return e->graphs.emplace(key, ge).first->second;
+}
+
+static bool device_loop_ok(const SlabGroup& g, int64_t ce, bool fused) {
+  const otfx_engine* e = g.lead();
+  return !g.local() && e->nranks == 1 && !fused && e->use_graphs && !e->timing && ce >= 2 &&
+         ce % 2 == 0 && env_int("OTFX_DEVICE_LOOP", 1) != 0;
+}
+
+// the run's full check periods from iteration `it` (a multiple of ce) on the
+// device; appends their history rows, returns false if the loop did not run
+static bool run_loop_device(otfx_engine* e, const otfx_run_config* cfg, double dn, int64_t& it,
+                            bool& conv) {
+  const int64_t ce = cfg->check_every;
+  const int64_t periods = (cfg->max_iters - it) / ce;
+  if (periods < 1) return false;
+  LoopCtl c = {};
+  c.tol_gap = cfg->tol_gap;
+  c.tol_feas = cfg->tol_feas;
+  c.diff_norm = dn;
+  c.it = it;
+  c.ce = ce;
+  c.periods_left = periods;
+  c.hist_cap = (long long)(e->stage_bytes / (6 * sizeof(double)));
+  cudaGraphExec_t ge = loop_graph(e, ce);
+  CK(cudaMemcpyAsync(e->d_loop, &c, sizeof(c), cudaMemcpyHostToDevice, e->stream));
+  CK(cudaGraphLaunch(ge, e->stream));
+  CK(cudaMemcpyAsync(&c, e->d_loop, sizeof(c), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  const size_t h0 = e->history.size();
+  e->history.resize(h0 + size_t(c.nh));
+  static_assert(sizeof(otfx_history_point) == 6 * sizeof(double), "history row layout");
+  CK(cudaMemcpyAsync(e->history.data() + h0, e->d_stage, size_t(c.nh) * sizeof(otfx_history_point),
+                     cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  it = c.it;
+  conv = c.conv != 0;
+  return true;
+}
+
 static void run_loop(const SlabGroup& g, const otfx_run_config* cfg, otfx_history_point* hist,
                      int64_t capacity, int64_t* n_history, int64_t* iterations, int* converged) {
   Range nv("otfx.run");
@@ -1772,6 +1895,10 @@ static void run_loop(const SlabGroup& g, const otfx_run_config* cfg, otfx_histor
   const int64_t ce = cfg->check_every, mx = cfg->max_iters;
   bool fused_ok = env_int("OTFX_FUSED_CHECK", 1) != 0;
   for (int q = 0; q < g.count; ++q) fused_ok = fused_ok && g.es[q]->use_tma;
+  if (!conv && device_loop_ok(g, ce, fused_ok)) {
+    Range nv("otfx.device_loop");
+    run_loop_device(e, cfg, dn, it, conv);
+  }
   while (!conv && it < mx) {
     const int64_t next = std::min((it / ce + 1) * ce, mx);
     group_plain(g, next - it - 1);

@@ -21,7 +21,7 @@ for n in (128, 256):
     eng.set_marginals(l0, l1)
     iters = 20000
     for ce in (100, iters):
-        eng.run(1e-300, 1e-300, 2 * ce if ce < iters else 200, ce)  # warm-up / graph capture
+        eng.run(1e-300, 1e-300, 2 * ce if ce < iters else iters, ce)  # warm-up / graph capture
         eng.zero_state()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
