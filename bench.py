@@ -404,8 +404,10 @@ def run_ours(args):
 
 def secondary_configs(args, device):
     """BASELINE configs[0..3] (the parity configurations) timed on the GPU
-    through the engine (device time, CUDA events) next to the NumPy port of the
-    reference on a bounded CPU sample.  Reported beside the headline, not as it."""
+    through the engine (device time, CUDA events) next to the reference itself
+    (baseline/_ref otflux, solve_* for a bounded number of iterations; the
+    NumPy port when it is not installed) on the box's host cores.  Reported
+    beside the headline, not as it."""
     import torch
     from threadpoolctl import threadpool_limits
 
@@ -457,31 +459,56 @@ def secondary_configs(args, device):
         torch.cuda.synchronize()
         gms = a.elapsed_time(b)
         eng.close()
-        # CPU: the NumPy port of the reference engine on a bounded sample
-        if kind == "vector":
-            ref = OracleEngine("vector", l0 - l1, n, cfg.tau, norm_u=cfg.norm_u.value,
-                               norm_w=cfg.norm_w.value, chan=graph.coefficients(),
-                               lam_chan=pk.lambda_max_graph(graph))
-        else:
-            mats = lind.matrices
-            diff = l0 - l1
-            dt = np.complex128 if complex_path else np.float64
-            ref = OracleEngine("matrix", diff if complex_path else np.ascontiguousarray(diff.real),
-                               n, cfg.tau, norm_u=cfg.norm_u.value, norm_w=cfg.norm_w.value,
-                               chan=mats if complex_path else np.ascontiguousarray(np.real(mats)),
-                               lam_chan=pk.lambda_max_L(lind), dtype=dt)
+        # CPU: the reference itself (baseline/_ref otflux, its public solve_*
+        # entry point for a bounded number of iterations, one check at the
+        # end) when installed, else the NumPy port of its engine
+        refmod = _import_reference()
         with threadpool_limits(limits=os.cpu_count() or 1):
-            ref.step()
-            t0 = time.perf_counter()
-            for _ in range(cpu_iters):
+            if refmod is not None:
+                otflux = refmod[0]
+                rcfg = otflux.SolverConfig(tau=cfg.tau, norm_u=cfg.norm_u.value,
+                                           norm_w=cfg.norm_w.value, alpha=1.0, tol_gap=1e-300,
+                                           tol_feas=1e-300, max_iters=cpu_iters,
+                                           check_every=cpu_iters)
+                if kind == "vector":
+                    args_ref = (otflux.VectorDensity(l0), otflux.VectorDensity(l1),
+                                otflux.triangle_graph())
+                    fn = otflux.solve_vector
+                else:
+                    args_ref = (otflux.MatrixDensity(l0), otflux.MatrixDensity(l1),
+                                otflux.LindbladSet(np.asarray(lind.matrices)))
+                    fn = otflux.solve_matrix
+                t0 = time.perf_counter()
+                rrep, _ = fn(*args_ref, cfg=rcfg)
+                cs = time.perf_counter() - t0
+                assert rrep.iterations == cpu_iters
+                cpu_kind = "reference"
+            else:
+                if kind == "vector":
+                    ref = OracleEngine("vector", l0 - l1, n, cfg.tau, norm_u=cfg.norm_u.value,
+                                       norm_w=cfg.norm_w.value, chan=graph.coefficients(),
+                                       lam_chan=pk.lambda_max_graph(graph))
+                else:
+                    mats = lind.matrices
+                    diff = l0 - l1
+                    dt = np.complex128 if complex_path else np.float64
+                    ref = OracleEngine("matrix", diff if complex_path else np.ascontiguousarray(diff.real),
+                                       n, cfg.tau, norm_u=cfg.norm_u.value, norm_w=cfg.norm_w.value,
+                                       chan=mats if complex_path else np.ascontiguousarray(np.real(mats)),
+                                       lam_chan=pk.lambda_max_L(lind), dtype=dt)
                 ref.step()
-            cs = time.perf_counter() - t0
+                t0 = time.perf_counter()
+                for _ in range(cpu_iters):
+                    ref.step()
+                cs = time.perf_counter() - t0
+                cpu_kind = "port"
         gpu_rate = n * n * it / (gms * 1e-3)
         cpu_rate = n * n * cpu_iters / cs
         row = dict(config=name, n=n, iterations=it, converged=conv,
                    final_primal=hist[-1].primal, gpu_seconds=gms * 1e-3,
                    gpu_cell_updates_per_s=gpu_rate, cpu_cell_updates_per_s=cpu_rate,
-                   cpu_sample_iterations=cpu_iters, speedup=gpu_rate / cpu_rate)
+                   cpu_sample_iterations=cpu_iters, cpu_kind=cpu_kind,
+                   speedup=gpu_rate / cpu_rate)
         if n == 256 and kind == "vector":
             # the whole reference run, timed once in the build container
             # (tools/make_c2_golden.py; the box cannot run 6 000 s per bench)
