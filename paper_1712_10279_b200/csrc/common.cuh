@@ -91,6 +91,11 @@ template <> __device__ __forceinline__ float tiny_of<float>() { return 0.0f; }
 
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
+// largest finite value of T
+template <typename T> __device__ __forceinline__ T FLT_MAX_OF();
+template <> __device__ __forceinline__ double FLT_MAX_OF<double>() { return 1.7976931348623157e308; }
+template <> __device__ __forceinline__ float FLT_MAX_OF<float>() { return 3.402823466e38f; }
+
 template <typename T>
 __device__ __forceinline__ T maxT(T a, T b) {
   // np.maximum semantics for the finite / inf values that occur here

@@ -344,6 +344,9 @@ __device__ void herm_jacobi(T (&ar)[K][K], T (&ai)[K][K], T (&vr)[K][K], T (&vi)
         if (!(r > T(0))) continue;
         // phase e^{-i phi} = conj(a_pq)/r
         const T rinv = T(1) / r;
+        // a subnormal |a_pq| (fp32 flux blocks decaying to 0) overflows 1/r:
+        // the pair is already diagonal to working precision
+        if (!(rinv <= FLT_MAX_OF<T>())) continue;
         const T er = ar[p][q] * rinv, ei = -ai[p][q] * rinv;
         const T zeta = (ar[q][q] - ar[p][p]) * (T(0.5) * rinv);
         const T t = (zeta >= T(0) ? T(1) : T(-1)) / (fabs(zeta) + sqrt(T(1) + zeta * zeta));

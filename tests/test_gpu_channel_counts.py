@@ -190,6 +190,39 @@ def test_matrix_runtime_size(monkeypatch, path, k, ell, cplx, norms):
     assert np.count_nonzero(st.w.values) > 0
 
 
+@pytest.mark.parametrize("kind", ["vector", "matrix"])
+def test_runtime_size_fp32(kind):
+    """The fp32 build of the runtime-size payloads: objective within 1e-4 of
+    the fp64 oracle at every check (the north star's fp32 bound)."""
+    rng = np.random.default_rng(11)
+    n, iters, ce = 24, 60, 20
+    if kind == "vector":
+        k = 12
+        graph = pk.TransportGraph(k, [(c, c + 1) for c in range(k - 1)], rng.uniform(0.5, 2.0, k - 1))
+        l0, l1 = _norm(rng, (n, n, k)), _norm(rng, (n, n, k))
+        cfg = pk.SolverConfig(tau=3.0, norm_u="l12", norm_w="l1", alpha=0.05, tol_gap=1e-300,
+                              tol_feas=1e-300, max_iters=iters, check_every=ce)
+        rep, st = pk.solve_vector(pk.VectorDensity(l0), pk.VectorDensity(l1), graph, cfg=cfg,
+                                  precision="f32")
+        eng = pdhg.OracleEngine("vector", l0 - l1, n, 3.0, norm_u="l12", norm_w="l1", alpha=0.05,
+                                chan=graph.coefficients(), lam_chan=pk.lambda_max_graph(graph))
+    else:
+        k, ell = 5, 3
+        a = rng.normal(size=(ell, k, k)) + 1j * rng.normal(size=(ell, k, k))
+        lind = pk.LindbladSet(0.5 * (a + np.conj(np.swapaxes(a, -1, -2))))
+        l0, l1 = _psd(rng, n, k, True), _psd(rng, n, k, True)
+        cfg = pk.SolverConfig(tau=10.0, norm_u="l1nuc", norm_w="l1nuc", alpha=0.3,
+                              tol_gap=1e-300, tol_feas=1e-300, max_iters=iters, check_every=ce)
+        rep, st = pk.solve_matrix(pk.MatrixDensity(l0), pk.MatrixDensity(l1), lind, cfg=cfg,
+                                  precision="f32")
+        eng = pdhg.OracleEngine("matrix", l0 - l1, n, 10.0, norm_u="l1nuc", norm_w="l1nuc",
+                                alpha=0.3, chan=lind.matrices, lam_chan=pk.lambda_max_L(lind),
+                                dtype=np.complex128)
+    _, _, hist = pdhg.oracle_run(eng, 1e-300, 1e-300, iters, ce)
+    assert rep.iterations == iters
+    assert g.rel_err(g.hist_array(rep)[:, 1], np.array(hist)[:, 1]) <= 1e-4
+
+
 def test_runtime_width_slabs_match_one_engine():
     """The runtime-size payload under the multi-slab run loop (overlapped
     halo exchange, NCCL loopback transport): the slabs' state equals one
