@@ -12,6 +12,7 @@ from .fields import (FluxField, GraphFlux, GridSpec, MatrixDensity, QuantumFlux,
                      VectorDensity, hermitian_part, normalize, skew_part, total_mass)
 from .graph import TransportGraph, lambda_max_graph, triangle_graph
 from .lindblad import LindbladSet, default_lindblad3, lambda_max_L, lindblad_pair_k2
+from .problems import dirac_pair, lambda_max_spatial_bound, matrix_blob_fixtures, rgb_disk_pair
 from .solver import (CudaEngine, HistoryPoint, NormFamily, SolveReport, SolverConfig, SolverState,
                      default_tau, duality_gap, residual_Rk, solve_matrix, solve_scalar,
                      solve_tensors, solve_vector, step_sizes_matrix, step_sizes_scalar, step_sizes_vector)
