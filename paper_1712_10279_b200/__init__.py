@@ -12,6 +12,8 @@ from .fields import (FluxField, GraphFlux, GridSpec, MatrixDensity, QuantumFlux,
                      VectorDensity, hermitian_part, normalize, skew_part, total_mass)
 from .graph import TransportGraph, lambda_max_graph, triangle_graph
 from .lindblad import LindbladSet, default_lindblad3, lambda_max_L, lindblad_pair_k2
+from .omtf import (load_graph, load_lindblad, read_density, read_omtf, save_graph, save_lindblad,
+                   write_omtf)
 from .problems import dirac_pair, lambda_max_spatial_bound, matrix_blob_fixtures, rgb_disk_pair
 from .solver import (CudaEngine, HistoryPoint, NormFamily, SolveReport, SolverConfig, SolverState,
                      default_tau, duality_gap, residual_Rk, solve_matrix, solve_scalar,
