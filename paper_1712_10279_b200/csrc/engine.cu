@@ -66,14 +66,14 @@ static int env_int(const char* name, int dflt) {
 template <>
 const Ops<double>* find_ops<double>(int kind, int K, int ell) {
   if (kind == KIND_SCALAR) return ops_vector_f64(1, false);
-  if (kind == KIND_VECTOR) return ops_vector_f64(K, true);
+  if (kind == KIND_VECTOR) return ops_vector_f64(K, true, ell);
   const Ops<double>* o = ops_matrix_f64(kind, K, ell);
   return o ? o : ops_matrix_dyn_f64(kind, K);
 }
 template <>
 const Ops<float>* find_ops<float>(int kind, int K, int ell) {
   if (kind == KIND_SCALAR) return ops_vector_f32(1, false);
-  if (kind == KIND_VECTOR) return ops_vector_f32(K, true);
+  if (kind == KIND_VECTOR) return ops_vector_f32(K, true, ell);
   const Ops<float>* o = ops_matrix_f32(kind, K, ell);
   return o ? o : ops_matrix_dyn_f32(kind, K);
 }

@@ -44,8 +44,10 @@ struct Ops {
 };
 
 // registries, one per instantiation unit
-const Ops<double>* ops_vector_f64(int K, bool has_w);
-const Ops<float>* ops_vector_f32(int K, bool has_w);
+// ell: edges of the graph (k >= 4 graphs with ell <= k take the sparse
+// instantiation, edge capacity k)
+const Ops<double>* ops_vector_f64(int K, bool has_w, int ell = 0);
+const Ops<float>* ops_vector_f32(int K, bool has_w, int ell = 0);
 const Ops<double>* ops_vector_dyn_f64(int K);  // k beyond the compiled policies
 const Ops<float>* ops_vector_dyn_f32(int K);
 const Ops<double>* ops_matrix_dyn_f64(int kind, int K);  // (k, ell) beyond the compiled ones

@@ -69,11 +69,15 @@ __device__ __forceinline__ T np_sumsq(const T* x, int len) {
 // vector / scalar payloads
 // ===========================================================================
 
-template <typename T, int K_, bool HASW>
+// LC_: edge capacity of the instantiation (0 = the complete graph's
+// k(k-1)/2); sparse graphs (chains, cycles, stars: ell <= k) get LC_ = k, so
+// the edge loops and the coefficient block are sized for the graph they run
+template <typename T, int K_, bool HASW, int LC_ = 0>
 struct VecPolicy {
   static constexpr int K = K_;
   static constexpr int NP = K;
-  static constexpr int LMAX = HASW ? (K * (K - 1) / 2 > 0 ? K * (K - 1) / 2 : 1) : 1;
+  static constexpr int LMAX =
+      HASW ? (LC_ > 0 ? LC_ : (K * (K - 1) / 2 > 0 ? K * (K - 1) / 2 : 1)) : 1;
   static constexpr int NWS = 1;                 // reals per channel block (edge)
   static constexpr int NW = HASW ? LMAX : 0;
   static constexpr int NWA = HASW ? LMAX : 1;   // array extent

@@ -56,7 +56,7 @@ struct TmaSweepArgs {
 // Channel coefficients as the kernels read them: the small vector D/c matrix
 // is pulled into registers once per CTA; the Lindblad stacks stay in the
 // (constant-cached) parameter space.
-template <class P, typename T, bool REG = (P::NCOEF > 0)>
+template <class P, typename T, bool REG = (P::NCOEF > 0 && P::NCOEF <= 64)>
 struct CoefView;
 template <class P, typename T>
 struct CoefView<P, T, true> {
