@@ -197,3 +197,35 @@ def test_host_prefault_touches_buffer_without_gpu():
     _lib.check(lib.otfx_host_prefault(None, 0))
     with pytest.raises(pk.ValidationError):
         _lib.check(lib.otfx_host_prefault(None, 8))
+
+
+def test_c_abi_header_compiles_and_links_from_c(tmp_path):
+    """include/otfx.h is plain C (C99, -Wall -Werror) and C++, and a C program
+    links against libotfx.so and calls into it -- the boundary a cgo / JNI /
+    ctypes binding of the reference would use (no device work: the ABI version
+    and the last-error string)."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    src = tmp_path / "abi.c"
+    src.write_text(
+        '#include <stdio.h>\n#include "otfx.h"\n'
+        "int main(void) {\n"
+        "  otfx_engine_desc d;\n"
+        "  (void)d;\n"
+        '  printf("%d %s\\n", otfx_abi_version(), otfx_last_error());\n'
+        "  return 0;\n}\n")
+    lib_dir = str(ROOT / "paper_1712_10279_b200")
+    inc = str(ROOT / "include")
+    exe = tmp_path / "abi"
+    for comp, std in (("gcc", "-std=c99"), ("g++", "-std=c++17")):
+        if shutil.which(comp) is None:
+            continue
+        subprocess.run([comp, std, "-Wall", "-Werror", "-x", "c" if comp == "gcc" else "c++",
+                        str(src), f"-I{inc}", f"-L{lib_dir}", "-l:libotfx.so",
+                        f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True, capture_output=True,
+                       text=True)
+        out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+        assert out.split()[0] == str(_lib.load().otfx_abi_version())
