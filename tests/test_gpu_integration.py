@@ -83,3 +83,32 @@ def test_reference_converged_solve_with_gpu_run(otflux_with_binding):
     assert rep.converged and rep_ref.converged
     assert rep.iterations == rep_ref.iterations
     assert rep.transport_value == pytest.approx(rep_ref.transport_value, rel=1e-10)
+
+
+def test_c_only_caller_matches_python_path(tmp_path):
+    """integration/otfx_scalar_example.c drives the engine through the C ABI
+    alone (create, set_marginals, run, history, destroy) on the reference's
+    Dirac-pair fixture (T/test_solver.py:70-77): same iteration count and the
+    same W1 bits as solve_scalar, and W1 = 0.5 within the reference's 2 %."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+
+    import paper_1712_10279_b200 as pk
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    root = Path(__file__).resolve().parent.parent
+    lib_dir = str(root / "paper_1712_10279_b200")
+    exe = tmp_path / "ex"
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", f"-I{root / 'include'}",
+                    str(root / "integration" / "otfx_scalar_example.c"), f"-L{lib_dir}",
+                    "-l:libotfx.so", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    iters, conv, w1 = int(out[0]), int(out[1]), float(out[2])
+    a, b = pk.dirac_pair(pk.GridSpec(33), (8, 16), (24, 16))
+    rep, _ = pk.solve_scalar(a, b, cfg=pk.SolverConfig(tau=3.0))
+    assert conv == 1 and rep.converged
+    assert iters == rep.iterations
+    assert w1 == rep.transport_value
+    assert abs(w1 - 0.5) <= 0.02 * 0.5

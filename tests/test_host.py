@@ -229,3 +229,18 @@ def test_c_abi_header_compiles_and_links_from_c(tmp_path):
                        text=True)
         out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
         assert out.split()[0] == str(_lib.load().otfx_abi_version())
+
+
+def test_c_example_builds(tmp_path):
+    """integration/otfx_scalar_example.c (a C-only caller of the engine) builds
+    against include/otfx.h and libotfx.so; tests/test_gpu_integration.py runs it."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    lib_dir = str(ROOT / "paper_1712_10279_b200")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", f"-I{ROOT / 'include'}",
+                    str(ROOT / "integration" / "otfx_scalar_example.c"), f"-L{lib_dir}",
+                    "-l:libotfx.so", f"-Wl,-rpath,{lib_dir}", "-o", str(tmp_path / "ex")],
+                   check=True, capture_output=True, text=True)
