@@ -1433,10 +1433,14 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     // (measured on B200: 2x2 complex l1nuc 75 % -> 88 % of the HBM roofline at
     // 3 stages / 3 CTAs vs 4 stages / 2 CTAs; fp32 vector, 3 CTAs either way:
     // 96 % at 4 stages vs 92 % at 3)
-    // (2 stages are a candidate only for the 6-warp heavy payloads)
+    // (2 stages: the 6-warp heavy payloads, and see below)
     const int wide = e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw;
     // (and for payloads whose 3-stage ring does not fit shared memory)
+    // (2 stages are also a candidate for the real-symmetric matrix payloads,
+    // where the shallower ring buys a third resident CTA: C4 family 2048^2
+    // 92.2 -> 94.0 % of the roofline; profiles/r02_stage_depth.txt)
     int smin = (wide == 6 && env_int("OTFX_TMA_WARPS", wide) == wide) ? 2 : 3;
+    if (d->kind == OTFX_KIND_MATRIX_REAL) smin = 2;
     if (smin == 3 && !plan_stages(e, 3)) smin = 2;
     int S = env_int("OTFX_STAGES", 0);
     if (S <= 0) {
@@ -1453,7 +1457,8 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
       }
       if (S <= 0) S = smin;
     }
-    e->use_tma = plan_stages(e, std::max(smin, S));
+    // (an explicit OTFX_STAGES >= 2 is honoured as given: measurement knob)
+    e->use_tma = plan_stages(e, env_int("OTFX_STAGES", 0) >= 2 ? S : std::max(smin, S));
   }
   if (e->use_tma) {
     e->gx = (n + e->L.tile - 1) / e->L.tile;
