@@ -1476,7 +1476,10 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     const int per_sm = std::max(1, e->ops64 ? e->ops64->tma_occupancy(e->L.cw, e->L.total)
                                             : e->ops32->tma_occupancy(e->L.cw, e->L.total));
     const long slots = (long)dev_sms * per_sm;
-    const int r0 = 16;
+    // (8 rows for the 2x2 complex payload: twice the CTAs, a smaller last
+    // wave -- C3 family 2048^2 0.2536 -> 0.2479 ms; 16 is best for the vector
+    // and real-symmetric ones, profiles/r02_stage_depth.txt)
+    const int r0 = (kind == OTFX_KIND_MATRIX_COMPLEX && e->K == 2) ? 8 : 16;
     int R = std::min(r0, e->rows);
     const long ctas = (long)e->gx * ((e->rows + R - 1) / R);
     const long waves = (ctas + slots - 1) / slots;
