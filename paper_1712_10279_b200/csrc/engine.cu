@@ -1491,6 +1491,19 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
       // to make the waves whole: 3x3 complex 1024^2, 6 x 64 CTAs (2.6 waves)
       // -> 6 x 74 (3 waves), l2/l1 0.264 -> 0.241 ms/iteration
       R = per_sm == 1 ? std::max(8, Rw) : std::max(R, Rw);
+    } else if (per_sm == 1) {
+      // many waves at one CTA per SM: the rows per CTA in [16, 32] whose CTA
+      // count fills its last wave best (3x3 complex l2/l1 2048^2: 10.4 waves
+      // at 16 rows -> 6.97 at 24, 0.781 -> 0.747 ms / iteration)
+      double best = -1.0;
+      for (int r = 16; r <= std::min(32, e->rows); ++r) {
+        const double w = double(e->gx * ((e->rows + r - 1) / r)) / double(slots);
+        const double fill = w / std::ceil(w);
+        if (fill > best + 1e-9) {
+          best = fill;
+          R = r;
+        }
+      }
     }
     e->R = env_int("OTFX_TILE_ROWS", R);
     e->gy = (e->rows + e->R - 1) / e->R;
