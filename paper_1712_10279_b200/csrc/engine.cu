@@ -335,6 +335,7 @@ struct otfx_engine {
   cudaEvent_t ev_hand = nullptr;  // caller-stream ordering of the device hand-off
   // TMA-streamed sweep
   bool use_tma = false;
+  bool narrow = false;  // 4 consumer warps although the payload has a wide instantiation
   // history of the last run() (the caller's buffer may be smaller: it gets
   // the first `capacity` rows, otfx_engine_history returns all of them)
   std::vector<otfx_history_point> history;
@@ -491,7 +492,7 @@ static bool plan_stages(otfx_engine* e, int S) {
   // columns, half the halo re-reads, for graph payloads; 6 for the heavy
   // complex matrices), else 4; OTFX_TMA_WARPS=4 overrides
   const int wide = e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw;
-  L.cw = env_int("OTFX_TMA_WARPS", wide) == wide ? wide : 4;
+  L.cw = (!e->narrow && env_int("OTFX_TMA_WARPS", wide) == wide) ? wide : 4;
   // the consumers hold stages q and q+1, so 2 is the minimum ring; only the
   // 6-warp heavy payloads use it (their stage is released before the W half
   // of the row, whose eigensolves cover the next load)
@@ -1426,8 +1427,15 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
   // TMA-streamed sweep: ring depth 4 (3 if that keeps two CTAs per SM)
   // the TMA ring pays off once rows are long enough to pipeline; small slabs
   // run the register-streamed sweep (measured: 4.4 vs 8.9 us/iteration at 64^2)
-  e->use_tma = env_int("OTFX_TMA", small ? 0 : 1) != 0 && !e->dynamic();
-  if (e->use_tma) {
+  const bool want_tma = env_int("OTFX_TMA", small ? 0 : 1) != 0 && !e->dynamic();
+  e->use_tma = want_tma;
+  // a wide (6 / 8-warp) plan that does not fit shared memory at any ring depth
+  // is retried with 4 consumer warps before falling back to the register
+  // sweep (4x4 complex, ell = 2: 1.45 -> 0.77 ms / iteration at 1024^2,
+  // profiles/r02_stage_depth.txt)
+  for (int attempt = 0; want_tma && attempt < 2; ++attempt) {
+    e->narrow = attempt == 1;
+    if (e->narrow && (e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw) == 4) break;
     // ring depth: 3 or 4 stages, whichever keeps more CTAs resident per SM
     // (registers and shared memory both count); on a tie the deeper ring
     // (measured on B200: 2x2 complex l1nuc 75 % -> 88 % of the HBM roofline at
@@ -1439,7 +1447,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     // (2 stages are also a candidate for the real-symmetric matrix payloads,
     // where the shallower ring buys a third resident CTA: C4 family 2048^2
     // 92.2 -> 94.0 % of the roofline; profiles/r02_stage_depth.txt)
-    int smin = (wide == 6 && env_int("OTFX_TMA_WARPS", wide) == wide) ? 2 : 3;
+    int smin = (wide == 6 && !e->narrow && env_int("OTFX_TMA_WARPS", wide) == wide) ? 2 : 3;
     if (d->kind == OTFX_KIND_MATRIX_REAL) smin = 2;
     if (smin == 3 && !plan_stages(e, 3)) smin = 2;
     int S = env_int("OTFX_STAGES", 0);
@@ -1459,6 +1467,7 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     }
     // (an explicit OTFX_STAGES >= 2 is honoured as given: measurement knob)
     e->use_tma = plan_stages(e, env_int("OTFX_STAGES", 0) >= 2 ? S : std::max(smin, S));
+    if (e->use_tma) break;
   }
   if (e->use_tma) {
     e->gx = (n + e->L.tile - 1) / e->L.tile;
