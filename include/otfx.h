@@ -125,6 +125,11 @@ int otfx_device_count(int* count);
  * blocks of every device to the driver. */
 int otfx_release_cached_memory(void);
 
+/* Payload sizes: scalar; vector k = 2..8 (compiled, any edge count) and
+ * k = 9..32 with up to 128 edges (runtime-size kernels); matrix k = 2..4 with
+ * ell <= 4 and k = 2, 3 with ell <= 8 (compiled), k <= 8 with ell * block
+ * reals <= 256 beyond that (runtime-size).  Anything else returns
+ * OTFX_EUNSUPPORTED before any device work. */
 int otfx_engine_create(const otfx_engine_desc* desc, otfx_engine** out);
 int otfx_engine_destroy(otfx_engine* e);
 int otfx_engine_get_info(otfx_engine* e, otfx_engine_info* info);
