@@ -10,8 +10,29 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace otfx {
+
+// Programmatic dependent launch.  Sweeps are launched with the
+// programmatic-stream-serialization attribute, so a sweep's CTAs are
+// rasterised and run their prologue (mbarrier init, parameter loads) while the
+// previous kernel of the stream drains; pdl_wait() then blocks until that
+// kernel has completed and its writes are visible, so every global read AND
+// write of the sweep (ping-pong state: it writes what its predecessor reads)
+// is ordered after it.  Outside a programmatic launch both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// host: OTFX_PDL=0 launches the sweeps without the attribute (A/B timing)
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* s = getenv("OTFX_PDL");
+    return !(s && atoi(s) == 0);
+  }();
+  return on;
+}
 
 // norm families, numbered as in include/otfx.h
 enum NormId : int { NORM_L2 = 0, NORM_L12 = 1, NORM_L1 = 2, NORM_L1NUC = 3 };

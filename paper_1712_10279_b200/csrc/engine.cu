@@ -417,6 +417,14 @@ const Ops<double>* ops_of<double>(otfx_engine* e) { return e->ops64; }
 template <>
 const Ops<float>* ops_of<float>(otfx_engine* e) { return e->ops32; }
 
+// threads per TMA sweep CTA: the 4-warp instantiation has a producer warp;
+// the wide one says (TmaRoles)
+static int tma_threads(const otfx_engine* e) {
+  const int wide = e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw;
+  if (e->L.cw != wide) return 32 * (e->L.cw + 1);
+  return e->ops64 ? e->ops64->wide_threads : e->ops32->wide_threads;
+}
+
 // fl bit 0: check sweep; bit 1: dual-norm accumulation (TMA sweep only).
 // One launch over nb bands (band0, band0 + step, ...) of the slab on stream s;
 // the iterate index is not advanced.
@@ -428,7 +436,7 @@ static void launch_bands(otfx_engine* e, int fl, int band0, int step, int nb, cu
     g.s.band0 = band0;
     g.s.band_step = step;
     g.L = e->L;
-    CK(ops_of<T>(e)->sweep_tma(g, e->maps[e->cur], dim3(e->gx, nb), dim3(32 * (e->L.cw + 1)), s,
+    CK(ops_of<T>(e)->sweep_tma(g, e->maps[e->cur], dim3(e->gx, nb), dim3(tma_threads(e)), s,
                                fl));
   } else {
     require((fl & 2) == 0, OTFX_EINVAL, "dual accumulation needs the TMA sweep");
@@ -489,17 +497,19 @@ static int round_up(int x, int a) { return (x + a - 1) / a * a; }
 static bool plan_stages(otfx_engine* e, int S) {
   StageLayout& L = e->L;
   // consumer warps per CTA: the payload's wide instantiation (8 warps, 248
-  // columns, half the halo re-reads, for graph payloads; 6 for the heavy
-  // complex matrices), else 4; OTFX_TMA_WARPS=4 overrides
+  // columns, half the halo re-reads, for graph payloads; 8 without a
+  // producer warp for the heavy complex matrices, 6 + producer at Lindblad
+  // capacity 4), else 4; OTFX_TMA_WARPS=4 overrides.  31 * cw columns of fp64
+  // must stay a multiple of 16 bytes (TMA box starts): cw even.
   const int wide = e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw;
   L.cw = (!e->narrow && env_int("OTFX_TMA_WARPS", wide) == wide) ? wide : 4;
   // the consumers hold stages q and q+1, so 2 is the minimum ring; only the
-  // 6-warp heavy payloads use it (their stage is released before the W half
+  // 8-warp heavy payloads use it (their stage is released before the W half
   // of the row, whose eigensolves cover the next load)
   require(S >= 2 && S <= 8, OTFX_EINVAL, "TMA ring depth out of range");
   L.tile = 31 * L.cw;  // a multiple of 16 bytes' worth of columns for fp32 and fp64
   L.h = 16 / e->elem;
-  L.tw = L.tile + 2 * L.h;
+  L.tw = round_up(L.tile + 2 * L.h, L.h);  // = StageShape::TW
   L.S = S;
   const int row = L.tw * e->elem;
   const int bu = 2 * e->NP * row, bw = e->NWact * row, bd = e->NP * row, bp = e->NP * row;
@@ -1441,13 +1451,14 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     // (measured on B200: 2x2 complex l1nuc 75 % -> 88 % of the HBM roofline at
     // 3 stages / 3 CTAs vs 4 stages / 2 CTAs; fp32 vector, 3 CTAs either way:
     // 96 % at 4 stages vs 92 % at 3)
-    // (2 stages: the 6-warp heavy payloads, and see below)
+    // (2 stages: the 8-warp heavy payloads, and see below)
     const int wide = e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw;
     // (and for payloads whose 3-stage ring does not fit shared memory)
     // (2 stages are also a candidate for the real-symmetric matrix payloads,
     // where the shallower ring buys a third resident CTA: C4 family 2048^2
     // 92.2 -> 94.0 % of the roofline; profiles/r02_stage_depth.txt)
-    int smin = (wide == 6 && !e->narrow && env_int("OTFX_TMA_WARPS", wide) == wide) ? 2 : 3;
+    const bool heavy = kind == OTFX_KIND_MATRIX_COMPLEX && e->K >= 3 && e->elem == 8;
+    int smin = (heavy && !e->narrow && env_int("OTFX_TMA_WARPS", wide) == wide) ? 2 : 3;
     if (d->kind == OTFX_KIND_MATRIX_REAL) smin = 2;
     if (smin == 3 && !plan_stages(e, 3)) smin = 2;
     int S = env_int("OTFX_STAGES", 0);
@@ -1492,27 +1503,26 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     int R = std::min(r0, e->rows);
     const long ctas = (long)e->gx * ((e->rows + R - 1) / R);
     const long waves = (ctas + slots - 1) / slots;
-    if (waves <= 8) {
-      const long gyw = std::max(1L, std::min<long>(waves * slots / e->gx, e->rows));
-      const int Rw = (int)((e->rows + gyw - 1) / gyw);
-      // at one resident CTA per SM (the 255-register heavy payloads) nothing
-      // back-fills a partial last wave, so rows per CTA may also shrink (to 8)
-      // to make the waves whole: 3x3 complex 1024^2, 6 x 64 CTAs (2.6 waves)
-      // -> 6 x 74 (3 waves), l2/l1 0.264 -> 0.241 ms/iteration
-      R = per_sm == 1 ? std::max(8, Rw) : std::max(R, Rw);
-    } else if (per_sm == 1) {
-      // many waves at one CTA per SM: the rows per CTA in [16, 32] whose CTA
-      // count fills its last wave best (3x3 complex l2/l1 2048^2: 10.4 waves
-      // at 16 rows -> 6.97 at 24, 0.781 -> 0.747 ms / iteration)
-      double best = -1.0;
-      for (int r = 16; r <= std::min(32, e->rows); ++r) {
-        const double w = double(e->gx * ((e->rows + r - 1) / r)) / double(slots);
-        const double fill = w / std::ceil(w);
-        if (fill > best + 1e-9) {
-          best = fill;
+    if (per_sm == 1) {
+      // one resident CTA per SM (the heavy payloads): nothing back-fills a
+      // partial wave, and every CTA re-derives its halo row's flux, so the
+      // sweep costs ~ (waves, rounded up) x (R + 1) row steps; take the R in
+      // [8, 32] that minimises it (3x3 complex 1024^2: R = 12, 3 whole waves;
+      // 2048^2: R = 32, 3.9 waves: l2/l1 0.645 -> 0.636 ms, l1nuc 0.659 ->
+      // 0.642 ms vs R = 16; profiles/r02_heavy_self8.md)
+      long best = -1;
+      for (int r = 8; r <= std::min(32, e->rows); ++r) {
+        const long w = (e->gx * ((e->rows + r - 1) / r) + slots - 1) / slots;
+        const long cost = w * (r + 1);
+        if (best < 0 || cost < best) {
+          best = cost;
           R = r;
         }
       }
+    } else if (waves <= 8) {
+      const long gyw = std::max(1L, std::min<long>(waves * slots / e->gx, e->rows));
+      const int Rw = (int)((e->rows + gyw - 1) / gyw);
+      R = std::max(R, Rw);
     }
     e->R = env_int("OTFX_TILE_ROWS", R);
     e->gy = (e->rows + e->R - 1) / e->R;

@@ -1,11 +1,32 @@
 // Builds an Ops<T> table entry for one payload policy.
 #pragma once
 
+#include <utility>
+
 #include "ops.h"
 #include "sweep.cuh"
 #include "sweep_tma.cuh"
 
 namespace otfx {
+
+// sweep launch with the programmatic-dependent-launch attribute (common.cuh
+// pdl_wait): the sweep's launch and prologue overlap the previous kernel's
+// tail -- the graph-node gap that dominates small grids
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_sweep_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem,
+                                    cudaStream_t s, Args&&... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 template <class P, typename T>
 struct OpsFor {
@@ -27,20 +48,30 @@ struct OpsFor {
     return cudaSuccess;
   }
   // wide CTAs (8 consumer warps, 248 columns) for the graph payloads.  The
-  // fp64 complex-Hermitian payloads with K >= 3 run at ptxas' 255-register cap,
-  // where registers allow 8 warps per SM but a 4-consumer CTA (+ producer)
-  // only 5 resident: they get 6 consumer warps (186 columns, a multiple of 16
-  // bytes of fp64) on a 2-stage ring.  The other matrix payloads keep 4.
-  static constexpr bool HEAVY = sizeof(T) == 8 && P::NCOEF == 0 && P::NP == P::K * P::K && P::K >= 3;
-  static constexpr int WIDE = (P::NCOEF > 0 || !P::HAS_W) ? 8 : (HEAVY ? 6 : 4);
+  // fp64 complex-Hermitian payloads with K >= 3 need 226-255 registers, so at
+  // most 8 warps fit an SM (two per sub-partition register file): they run 8
+  // consumer warps with no producer warp (the last warp to release a ring slot
+  // refills it, TmaRoles) on a 2-stage ring, one CTA per SM -- 3x3 complex
+  // 2048^2 0.743 -> 0.648 ms (l2/l1) / 0.662 ms (l1nuc), profiles/
+  // r02_heavy_self8.md (6 consumer warps + producer before).  The other
+  // matrix payloads keep 4.
+  static constexpr bool HEAVY = TmaRoles<P, T, 4>::HEAVY;
+#ifndef OTFX_HEAVY_CW
+#define OTFX_HEAVY_CW 8
+#endif
+  // (Lindblad capacity 4: a 72-plane stage fits a 2-stage ring only at 6
+  // consumer warps, which keep their producer warp)
+  static constexpr int WIDE =
+      (P::NCOEF > 0 || !P::HAS_W) ? 8 : (HEAVY ? (P::LMAX <= 2 ? OTFX_HEAVY_CW : 6) : 4);
   template <int CW>
   static void launch_tma(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
                          cudaStream_t s, int fl) {
+    const size_t sm = a.L.total;
     switch (fl & 3) {
-      case 0: sweep_tma_kernel<P, T, 0, CW><<<g, b, a.L.total, s>>>(a, m); break;
-      case 1: sweep_tma_kernel<P, T, 1, CW><<<g, b, a.L.total, s>>>(a, m); break;
-      case 2: sweep_tma_kernel<P, T, 2, CW><<<g, b, a.L.total, s>>>(a, m); break;
-      default: sweep_tma_kernel<P, T, 3, CW><<<g, b, a.L.total, s>>>(a, m); break;
+      case 0: launch_sweep_pdl(sweep_tma_kernel<P, T, 0, CW>, g, b, sm, s, a, m); break;
+      case 1: launch_sweep_pdl(sweep_tma_kernel<P, T, 1, CW>, g, b, sm, s, a, m); break;
+      case 2: launch_sweep_pdl(sweep_tma_kernel<P, T, 2, CW>, g, b, sm, s, a, m); break;
+      default: launch_sweep_pdl(sweep_tma_kernel<P, T, 3, CW>, g, b, sm, s, a, m); break;
     }
   }
   static cudaError_t sweep_tma(const TmaSweepArgs<T>& a, const TmaSet& m, dim3 g, dim3 b,
@@ -64,8 +95,8 @@ struct OpsFor {
   static int tma_occupancy(int cw, size_t smem) {
     int nb = 0;
     if (cw == WIDE)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_tma_kernel<P, T, 0, WIDE>, 32 * (WIDE + 1),
-                                                    smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_tma_kernel<P, T, 0, WIDE>,
+                                                    TmaRoles<P, T, WIDE>::THREADS, smem);
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_tma_kernel<P, T, 0, 4>, 160, smem);
     return nb;
@@ -77,11 +108,8 @@ struct OpsFor {
   }
   static cudaError_t sweep(const SweepArgs<T>& a, dim3 g, dim3 b, size_t smem, cudaStream_t s,
                            bool check) {
-    if (check)
-      sweep_kernel<P, T, true><<<g, b, smem, s>>>(a);
-    else
-      sweep_kernel<P, T, false><<<g, b, smem, s>>>(a);
-    return cudaGetLastError();
+    if (check) return launch_sweep_pdl(sweep_kernel<P, T, true>, g, b, smem, s, a);
+    return launch_sweep_pdl(sweep_kernel<P, T, false>, g, b, smem, s, a);
   }
   // the on-chip cluster solve is instantiated for the graph / scalar payloads
   static constexpr bool CLUSTER = (P::NCOEF > 0 || !P::HAS_W);
@@ -152,7 +180,7 @@ struct OpsFor {
     static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
                              P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &sweep_tma,
                              &regs, &tma_regs,
-                             WIDE,     &tma_occupancy, &sweep_occupancy,
+                             WIDE,     TmaRoles<P, T, WIDE>::THREADS, &tma_occupancy, &sweep_occupancy,
                              CLUSTER ? &cluster_run : nullptr, &cluster_smem, &cluster_fits};
     return &o;
   }

@@ -422,6 +422,48 @@ __device__ void herm_nuc_prox(T (&hr)[K][K], T (&hi)[K][K], T thr) {
     hi[1][0] = -hi[0][1];
     hi[0][0] = hi[1][1] = T(0);
   } else {
+  // Spectral enclosure first: with m = tr X / K every eigenvalue lies within
+  // rho = sqrt((K-1)/K) ||X - m I||_F of m.  When the whole interval
+  // [m - rho, m + rho] is on one piece of the soft threshold, the prox is
+  // X - thr I, X + thr I or 0 without an eigensolve (the reference's
+  // V diag(f) V^H equals these to rounding).  The enclosure is widened by a
+  // relative 1e-12 so rounding in rho cannot put a boundary eigenvalue on
+  // the wrong piece; cells on the boundary take the Jacobi path.
+#ifndef OTFX_NUC_ENCLOSURE
+#define OTFX_NUC_ENCLOSURE 1
+#endif
+  if (OTFX_NUC_ENCLOSURE) {
+    T tr = T(0);
+#pragma unroll
+    for (int a = 0; a < K; ++a) tr = tr + hr[a][a];
+    const T m = tr * (T(1) / T(K));
+    T f2 = T(0);
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      const T d = hr[a][a] - m;
+      f2 = fma(d, d, f2);
+#pragma unroll
+      for (int b = a + 1; b < K; ++b) f2 = fma(T(2) * hr[a][b], hr[a][b], fma(T(2) * hi[a][b], hi[a][b], f2));
+    }
+    const T rho = sqrt(f2 * (T(K - 1) / T(K))) * T(1 + 1e-12) + fabs(m) * T(1e-12);
+    const int piece = (m - rho > thr) ? 1 : ((m + rho < -thr) ? -1 : ((m + rho < thr && m - rho > -thr) ? 0 : 2));
+    if (piece != 2) {
+      const T sh = piece == 1 ? -thr : thr;
+#pragma unroll
+      for (int a = 0; a < K; ++a)
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          if (piece == 0) {
+            hr[a][b] = T(0);
+            hi[a][b] = T(0);
+          } else if (a == b) {
+            hr[a][b] = hr[a][b] + sh;
+            hi[a][b] = T(0);
+          }
+        }
+      return;
+    }
+  }
   T ar[K][K], ai[K][K], vr[K][K], vi[K][K];
 #pragma unroll
   for (int a = 0; a < K; ++a)

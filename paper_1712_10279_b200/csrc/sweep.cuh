@@ -161,6 +161,8 @@ __global__ void __launch_bounds__(128, ((P::NCOEF > 0 || !P::HAS_W) && P::K <= 3
   // row's inputs, phi of rows gr0 and gr0-1, u of row gr0-1): small grids run
   // one row per CTA, where a chain of dependent load rounds is the latency.
   RowIn in;
+  pdl_wait();  // the previous sweep has finished reading what this one writes
+  pdl_launch_dependents();
   load_row(gr0, in);
   {
     const int64_t o = cell_off(A, gr0, j);

@@ -96,7 +96,9 @@ struct StageShape {
   static constexpr int CW = CW_;                    // consumer warps per CTA
   static constexpr int H = 16 / int(sizeof(T));     // halo columns (16 B)
   static constexpr int TILE = 31 * CW;              // output columns per CTA
-  static constexpr int TW = TILE + 2 * H;           // staged columns
+  // staged columns, a multiple of 16 bytes (TMA box rows; an odd warp count
+  // stages one spare column)
+  static constexpr int TW = (TILE + 2 * H + H - 1) / H * H;
   static constexpr int ROW = TW * int(sizeof(T));
   static constexpr int R128(int x) { return (x + 127) / 128 * 128; }
   static constexpr int OFF_W = R128(2 * P::NP * ROW);
@@ -105,53 +107,75 @@ struct StageShape {
   static constexpr int BYTES = OFF_P + R128(P::NP * ROW);
 };
 
-// The producer warp's loop (one elected lane): stage q of the ring gets
-// global row qbase + q -- the halo row (u, phi), the R owned rows (u, w, diff,
-// phi), the phi-only tail row -- each a set of 3-D TMA boxes completing on
-// full[slot]; a slot is reused once every consumer warp has arrived on
-// empty[slot].
+// Loads of ring stage q (global row qbase + q) into `slot`: the halo row
+// (u, phi), the R owned rows (u, w, diff, phi), the phi-only tail row -- each
+// a set of 3-D TMA boxes completing on full[slot].
+template <class SS, class P, typename T>
+__device__ __forceinline__ void tma_issue_stage(const SweepArgs<T>& A, const StageLayout& L,
+                                                const TmaSet& M, uint64_t* full,
+                                                unsigned char* stages, int c0, int gr0, int qbase,
+                                                int qmax, int q, int slot) {
+  const int n = A.n;
+  const int cx = c0 - SS::H;
+  uint64_t* bar = &full[slot];
+  const int r = qbase + q;
+  const int lrow = r - A.row_begin + 1;
+  unsigned char* st = stages + slot * SS::BYTES;
+  if (q == 0 || q == qmax) {
+    const bool load = (q == 0) ? (gr0 > 0) : (r < n);
+    if (!load) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+    } else {
+      if (q == 0) {
+        mbar_expect_tx(bar, L.bytes_flux);
+        tma_load_3d(st, &M.u, bar, cx, lrow, 0);
+      } else {
+        mbar_expect_tx(bar, L.bytes_phi);
+      }
+      tma_load_3d(st + SS::OFF_P, &M.phi, bar, cx, lrow, 0);
+    }
+  } else {
+    mbar_expect_tx(bar, L.bytes_full);
+    tma_load_3d(st, &M.u, bar, cx, lrow, 0);
+    if (P::HAS_W) tma_load_3d(st + SS::OFF_W, &M.w, bar, cx, lrow, 0);
+    tma_load_3d(st + SS::OFF_D, &M.diff, bar, cx, lrow, 0);
+    tma_load_3d(st + SS::OFF_P, &M.phi, bar, cx, lrow, 0);
+  }
+}
+
+// The producer warp's loop (one elected lane): stage q of the ring is reused
+// once every consumer warp has arrived on empty[slot].
 template <class SS, class P, typename T>
 __device__ __forceinline__ void tma_produce(const SweepArgs<T>& A, const StageLayout& L,
                                             const TmaSet& M, uint64_t* full, uint64_t* empty,
                                             unsigned char* stages, int c0, int gr0, int gr1,
                                             int qbase, int qmax) {
   const int S = L.S;
-  const int n = A.n;
-
-  const int cx = c0 - SS::H;
   int slot = 0, use = 0;
   for (int q = 0; q <= qmax; ++q) {
     if (q >= S) mbar_wait(&empty[slot], (use - 1) & 1);
-    uint64_t* bar = &full[slot];
-    const int r = qbase + q;
-    const int lrow = r - A.row_begin + 1;
-    unsigned char* st = stages + slot * SS::BYTES;
-    if (q == 0 || q == qmax) {
-      const bool load = (q == 0) ? (gr0 > 0) : (r < n);
-      if (!load) {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-      } else {
-        if (q == 0) {
-          mbar_expect_tx(bar, L.bytes_flux);
-          tma_load_3d(st, &M.u, bar, cx, lrow, 0);
-        } else {
-          mbar_expect_tx(bar, L.bytes_phi);
-        }
-        tma_load_3d(st + SS::OFF_P, &M.phi, bar, cx, lrow, 0);
-      }
-    } else {
-      mbar_expect_tx(bar, L.bytes_full);
-      tma_load_3d(st, &M.u, bar, cx, lrow, 0);
-      if (P::HAS_W) tma_load_3d(st + SS::OFF_W, &M.w, bar, cx, lrow, 0);
-      tma_load_3d(st + SS::OFF_D, &M.diff, bar, cx, lrow, 0);
-      tma_load_3d(st + SS::OFF_P, &M.phi, bar, cx, lrow, 0);
-    }
+    tma_issue_stage<SS, P, T>(A, L, M, full, stages, c0, gr0, qbase, qmax, q, slot);
     if (++slot == S) {
       slot = 0;
       ++use;
     }
   }
 }
+
+#ifndef OTFX_HEAVY_SELF
+#define OTFX_HEAVY_SELF 1
+#endif
+// Thread roles of a TMA sweep CTA: CW consumer warps plus one producer warp,
+// except (OTFX_HEAVY_SELF, default on) the wide heavy complex-Hermitian payloads, whose
+// 255-register consumers fit at most 8 warps per SM (2 per sub-partition's
+// register file): there the last consumer warp to release a ring slot issues
+// the slot's next loads itself, and all 8 warps compute.
+template <class P, typename T, int CW>
+struct TmaRoles {
+  static constexpr bool HEAVY = sizeof(T) == 8 && P::NCOEF == 0 && P::NP == P::K * P::K && P::K >= 3;
+  static constexpr bool SELF = OTFX_HEAVY_SELF != 0 && HEAVY && CW == 8;
+  static constexpr int THREADS = 32 * (CW + (SELF ? 0 : 1));
+};
 
 // FL bit 0 (CHECK): this sweep ends on a check iteration -- accumulate the
 //   R^k terms (S/solver.py:282-291) from the old and new values in registers;
@@ -171,7 +195,7 @@ template <class P, typename T, int FL, int CWT = 4>
 // The 4-warp instantiations (matrix payloads) keep ptxas' default (0 = no
 // hint): stating minBlocks = 1 there raises the 3x3 real payload from 156 to
 // 196 registers and halves its occupancy.
-__global__ void __launch_bounds__(32 * (CWT + 1),
+__global__ void __launch_bounds__(TmaRoles<P, T, CWT>::THREADS,
                                   (CWT == 8 && (P::NCOEF > 0 || !P::HAS_W)) ? (FL != 0 ? 2 : 1) : 0)
     sweep_tma_kernel(
     const __grid_constant__ TmaSweepArgs<T> G, const __grid_constant__ TmaSet M) {
@@ -193,7 +217,9 @@ __global__ void __launch_bounds__(32 * (CWT + 1),
   const int S = L.S;
   const int t = threadIdx.x;
   const int warp = t >> 5, lane = t & 31;
-  const bool producer = warp >= CW;
+  constexpr bool SELF = TmaRoles<P, T, CWT>::SELF;
+  const bool producer = !SELF && warp >= CW;
+  int* cnt = reinterpret_cast<int*>(empty);  // SELF: releases per slot
   const int c0 = blockIdx.x * SS::TILE;
   const int sc = SS::H + 31 * warp + lane - 1;  // staged column index of this thread's column
   const int j = c0 - SS::H + sc;                // = c0 + 31 warp + lane - 1
@@ -209,11 +235,18 @@ __global__ void __launch_bounds__(32 * (CWT + 1),
   if (t == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CW);
+      if (SELF) cnt[2 * s] = 0;
+      else mbar_init(&empty[s], CW);
     }
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();  // the previous sweep has finished reading what this one writes
+  pdl_launch_dependents();
+  if (SELF && t == 0) {
+    for (int q = 0; q < S && q <= qmax; ++q)
+      tma_issue_stage<SS, P, T>(A, L, M, full, stages, c0, gr0, qbase, qmax, q, q);
+  }
 
   // CHECK: SDU SDW SDPHI SCROSS;  DUAL: PU PW SU2 SW2 SCON SPHID PENU PENW | GU GW
   double acc[4] = {0, 0, 0, 0};
@@ -237,11 +270,27 @@ __global__ void __launch_bounds__(32 * (CWT + 1),
     auto base = [&](int s) -> const T* {
       return reinterpret_cast<const T*>(stages + s * SS::BYTES) + sc;
     };
+    int qrel = 0;  // ring stage released next
     auto release = [&](int s) {
       __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
-                     : "memory");
+      if (lane == 0) {
+        if constexpr (SELF) {
+          // the last warp out refills the slot with stage qrel + S
+          __threadfence_block();
+          if (atomicAdd(&cnt[2 * s], 1) == CW - 1) {
+            atomicExch(&cnt[2 * s], 0);
+            const int qn = qrel + S;
+            if (qn <= qmax) {
+              fence_proxy_async();
+              tma_issue_stage<SS, P, T>(A, L, M, full, stages, c0, gr0, qbase, qmax, qn, s);
+            }
+          }
+        } else {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s]))
+                       : "memory");
+        }
+      }
+      ++qrel;
     };
     T uxb_prev[NP], dux_prev[NP], uox_prev[NP];
 #pragma unroll
@@ -320,6 +369,16 @@ __global__ void __launch_bounds__(32 * (CWT + 1),
           if (DUAL) luo[c] = __shfl_up_sync(0xffffffffu, uo[1][c], 1);
         }
       }
+      // u' is final: store it now, so its registers are free for the channel
+      // half of the row (the heavy complex payloads run at the register cap)
+      if (out) {
+        T* pu = gu + cell_off(A, i, j);
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          pu[c * pl] = un[0][c];
+          pu[(NP + c) * pl] = un[1][c];
+        }
+      }
       T df[NP], wo[NWA];
 #pragma unroll
       for (int c = 0; c < NP; ++c) df[c] = sD[c * TW];
@@ -354,6 +413,10 @@ __global__ void __launch_bounds__(32 * (CWT + 1),
             wb[e] = (wn[e] + wn[e]) - wo[e];
             dwv[e] = wn[e] - wo[e];
           }
+          T* pw = gw + o;
+#pragma unroll
+          for (int e = 0; e < NWA; ++e)
+            if (e < nwp) pw[e * pl] = wn[e];
           P::div_c(wb, dv, H);
 #pragma unroll
           for (int c = 0; c < NP; ++c) rhs[c] = rhs[c] + dv[c];
@@ -364,20 +427,9 @@ __global__ void __launch_bounds__(32 * (CWT + 1),
           rhs[c] = rhs[c] * H.tau;
           phnew[c] = phc[c] + rhs[c];
         }
-        T* pu = gu + o;
         T* pp = gphi + o;
 #pragma unroll
-        for (int c = 0; c < NP; ++c) {
-          pu[c * pl] = un[0][c];
-          pu[(NP + c) * pl] = un[1][c];
-          pp[c * pl] = phnew[c];
-        }
-        if (P::HAS_W) {
-          T* pw = gw + o;
-#pragma unroll
-          for (int e = 0; e < NWA; ++e)
-            if (e < nwp) pw[e * pl] = wn[e];
-        }
+        for (int c = 0; c < NP; ++c) pp[c * pl] = phnew[c];
         if (CHECK) {
           T cross[NP];
 #pragma unroll

@@ -33,7 +33,7 @@ for name, (n, gen, lind, norms, cplx, iters) in cases.items():
     eng.close()
 print(json.dumps(out))
 '''
-variants = [{}, {"OTFX_TILE_COLS": "64"}, {"OTFX_TILE_COLS": "32"}, {"OTFX_TILE_ROWS": "2"},
+variants = [json.loads(a) for a in sys.argv[1:]] or [{}, {"OTFX_TILE_COLS": "64"}, {"OTFX_TILE_COLS": "32"}, {"OTFX_TILE_ROWS": "2"},
             {"OTFX_TMA": "1"}, {"OTFX_TMA": "1", "OTFX_TILE_ROWS": "2"},
             {"OTFX_TMA": "1", "OTFX_TILE_ROWS": "4"}, {"OTFX_GRAPHS": "0"}]
 for env in variants:
