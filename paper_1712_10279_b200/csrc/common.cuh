@@ -89,6 +89,7 @@ struct SweepArgs {
   T mu, thr_w, tau, nu, inv_dx;
   T den_u, den_w;        // (1 + 2 mu eps), (1 + 2 thr_w eps/alpha); 1 when eps == 0
   int has_eps;
+  int real_l;            // complex matrix path: every Lindblad operator is real
   double alpha, eps;
   double* partials;      // CHECK sweeps: [blocks][10]; evaluate: [blocks][8]
   double* maxes;         // evaluate: [blocks][2]

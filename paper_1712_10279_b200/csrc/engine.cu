@@ -406,6 +406,13 @@ static SweepArgs<T> make_args(otfx_engine* e, int from) {
       for (int q = 0; q < e->d.ell; ++q) a.coef[c * L + q] = e->chan[size_t(c) * e->d.ell + q];
   } else if (e->d.kind != OTFX_KIND_SCALAR) {
     for (size_t q = 0; q < e->chan.size(); ++q) a.coef[q] = e->chan[q];
+    if (e->d.kind == OTFX_KIND_MATRIX_COMPLEX) {
+      // real Lindblad stacks (the DTI and Pauli-x sets) skip the imaginary
+      // multiply-adds of the commutators (HermPolicy lmac / macl)
+      a.real_l = env_int("OTFX_REAL_L", 1) != 0 ? 1 : 0;
+      for (size_t q = 1; q < e->chan.size(); q += 2)
+        if (e->chan[q] != 0.0) a.real_l = 0;
+    }
   }
   return a;
 }

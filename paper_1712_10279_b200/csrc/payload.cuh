@@ -938,9 +938,40 @@ struct HermPolicy {
     return {T(A.coef[o]), T(A.coef[o + 1])};
   }
 
+  // L_s(a, b) times x (lmac) or x times L_s(a, b) (macl).  RL: the stack is
+  // real (A.real_l), so the imaginary parts are not read and their
+  // multiply-adds are not issued -- the same values as the complex form,
+  // whose terms with a zero imaginary part add exactly 0 (up to the sign of
+  // a zero)
+  template <bool RL, class PA>
+  __device__ static __forceinline__ cpx<T> lmac(cpx<T> acc, const PA& A, int s, int a, int b,
+                                                cpx<T> x) {
+    if constexpr (RL) {
+      const T lr = T(A.coef[((s * K + a) * K + b) * 2]);
+      return {fma(lr, x.r, acc.r), fma(lr, x.i, acc.i)};
+    } else {
+      return cmac(acc, L(A, s, a, b), x);
+    }
+  }
+  template <bool RL, class PA>
+  __device__ static __forceinline__ cpx<T> macl(cpx<T> acc, cpx<T> z, const PA& A, int s, int a,
+                                                int b) {
+    if constexpr (RL) {
+      const T lr = T(A.coef[((s * K + a) * K + b) * 2]);
+      return {fma(z.r, lr, acc.r), fma(z.i, lr, acc.i)};
+    } else {
+      return cmac(acc, z, L(A, s, a, b));
+    }
+  }
+
   // [L_s, X] = P - P^H, P = L_s X
   template <class PA>
   __device__ static void grad_c(const T (&p)[NP], T (&g)[NWA], const PA& A) {
+    if (A.real_l) grad_c_impl<true>(p, g, A);
+    else grad_c_impl<false>(p, g, A);
+  }
+  template <bool RL, class PA>
+  __device__ static __forceinline__ void grad_c_impl(const T (&p)[NP], T (&g)[NWA], const PA& A) {
     T xr[K][K], xi[K][K];
     unpack_h(p, xr, xi);
 #pragma unroll
@@ -952,7 +983,7 @@ struct HermPolicy {
         for (int b = 0; b < K; ++b) {
           cpx<T> acc = {T(0), T(0)};
 #pragma unroll
-          for (int c = 0; c < K; ++c) acc = cmac(acc, L(A, s, a, c), cpx<T>{xr[c][b], xi[c][b]});
+          for (int c = 0; c < K; ++c) acc = lmac<RL>(acc, A, s, a, c, cpx<T>{xr[c][b], xi[c][b]});
           P[a][b] = acc;
         }
       T* z = &g[s * NWS];
@@ -972,6 +1003,11 @@ struct HermPolicy {
   // T + T^H, T = sum_s Z_s L_s
   template <class PA>
   __device__ static void div_c(const T (&y)[NWA], T (&d)[NP], const PA& A) {
+    if (A.real_l) div_c_impl<true>(y, d, A);
+    else div_c_impl<false>(y, d, A);
+  }
+  template <bool RL, class PA>
+  __device__ static __forceinline__ void div_c_impl(const T (&y)[NWA], T (&d)[NP], const PA& A) {
     cpx<T> Tm[K][K];
 #pragma unroll
     for (int a = 0; a < K; ++a)
@@ -997,7 +1033,7 @@ struct HermPolicy {
         for (int b = 0; b < K; ++b) {
           cpx<T> acc = Tm[a][b];
 #pragma unroll
-          for (int c = 0; c < K; ++c) acc = cmac(acc, Z[a][c], L(A, s, c, b));
+          for (int c = 0; c < K; ++c) acc = macl<RL>(acc, Z[a][c], A, s, c, b);
           Tm[a][b] = acc;
         }
     }

@@ -79,12 +79,12 @@ struct CoefView<P, T, false> {
 template <class P, typename T>
 struct HotArgs {
   T mu, thr_w, nu, tau, inv_dx, den_u, den_w;
-  int has_eps, norm_u, norm_w, ell;
+  int has_eps, norm_u, norm_w, ell, real_l;
   double alpha;
   CoefView<P, T> coef;
   __device__ __forceinline__ void load(const SweepArgs<T>& A) {
     mu = A.mu; thr_w = A.thr_w; nu = A.nu; tau = A.tau; inv_dx = A.inv_dx;
-    den_u = A.den_u; den_w = A.den_w; has_eps = A.has_eps;
+    den_u = A.den_u; den_w = A.den_w; has_eps = A.has_eps; real_l = A.real_l;
     norm_u = A.norm_u; norm_w = A.norm_w; ell = A.ell; alpha = A.alpha;
     coef.load(A);
   }
