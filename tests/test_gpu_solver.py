@@ -530,6 +530,38 @@ def test_tma_heavy_complex_widths_identical(monkeypatch, warps):
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("n,rows", [(40, 1), (40, 3), (257, 1), (257, 5)])
+def test_tma_heavy_self_produce_ragged(monkeypatch, n, rows):
+    """8-warp self-producing ring (no producer warp: the last warp out of a
+    slot issues its next stage) on ragged shapes -- one-row CTAs whose ring
+    holds the whole band, a partial last CTA column, rows not dividing n --
+    bit-identical to the register sweep, with checks (fused check and dual
+    sweeps) on the way."""
+    l0, l1 = synthetic.matrix_blob_fixtures(n)[:2]
+    cfg = pk.SolverConfig(tau=30.0, norm_u="l1nuc", norm_w="l2", tol_gap=1e-300,
+                          tol_feas=1e-300, max_iters=14, check_every=5)
+    outs = []
+    for tma in ("1", "0"):
+        monkeypatch.setenv("OTFX_TMA", tma)
+        if tma == "1":
+            monkeypatch.setenv("OTFX_TILE_ROWS", str(rows))
+        else:
+            monkeypatch.delenv("OTFX_TILE_ROWS", raising=False)
+        eng = build_engine("matrix", n, cfg, lindblad=pk.default_lindblad3(), complex_path=True)
+        if tma == "1":
+            inf = eng.info()
+            assert inf["tile_cols"] == 248 and inf["tile_rows"] == rows
+        eng.set_marginals(l0, l1)
+        h, it, conv, _ = eng.run(cfg.tol_gap, cfg.tol_feas, cfg.max_iters, cfg.check_every)
+        outs.append((eng.get_state(), [(r.iteration, r.primal, r.dual, r.gap_ratio,
+                                         r.feas_residual, r.residual) for r in h]))
+        eng.close()
+    for a, b in zip(outs[0][0], outs[1][0]):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_allclose(np.array(outs[0][1], dtype=float), np.array(outs[1][1], dtype=float),
+                               rtol=1e-12, atol=0)
+
+
 # ---------------------------------------------------------------------------
 # on-chip cluster solve (small grids: whole run loop in one cluster launch)
 # against the streamed per-iteration path: same iterates bit for bit, same
