@@ -72,6 +72,7 @@ struct DynOps {
     o->tma_regs = &no_regs;
     o->wide_cw = 4;
     o->wide_threads = 160;
+    o->narrow_threads = 160;
     o->tma_occupancy = &no_occupancy;
     o->sweep_occupancy = &sweep_occupancy;
     o->cluster_run = nullptr;

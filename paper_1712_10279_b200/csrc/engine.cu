@@ -428,7 +428,7 @@ const Ops<float>* ops_of<float>(otfx_engine* e) { return e->ops32; }
 // the wide one says (TmaRoles)
 static int tma_threads(const otfx_engine* e) {
   const int wide = e->ops64 ? e->ops64->wide_cw : e->ops32->wide_cw;
-  if (e->L.cw != wide) return 32 * (e->L.cw + 1);
+  if (e->L.cw != wide) return e->ops64 ? e->ops64->narrow_threads : e->ops32->narrow_threads;
   return e->ops64 ? e->ops64->wide_threads : e->ops32->wide_threads;
 }
 
@@ -1467,6 +1467,8 @@ static void create(const otfx_engine_desc* d, otfx_engine* e) {
     const bool heavy = kind == OTFX_KIND_MATRIX_COMPLEX && e->K >= 3 && e->elem == 8;
     int smin = (heavy && !e->narrow && env_int("OTFX_TMA_WARPS", wide) == wide) ? 2 : 3;
     if (d->kind == OTFX_KIND_MATRIX_REAL) smin = 2;
+    // (self-producing 4-warp CTAs: a 2-stage ring buys the fourth resident CTA)
+    if ((e->ops64 ? e->ops64->narrow_threads : e->ops32->narrow_threads) == 128) smin = 2;
     if (smin == 3 && !plan_stages(e, 3)) smin = 2;
     int S = env_int("OTFX_STAGES", 0);
     if (S <= 0) {

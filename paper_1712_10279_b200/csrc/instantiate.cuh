@@ -98,7 +98,8 @@ struct OpsFor {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_tma_kernel<P, T, 0, WIDE>,
                                                     TmaRoles<P, T, WIDE>::THREADS, smem);
     else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_tma_kernel<P, T, 0, 4>, 160, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sweep_tma_kernel<P, T, 0, 4>,
+                                                    TmaRoles<P, T, 4>::THREADS, smem);
     return nb;
   }
   static int sweep_occupancy(int threads, size_t smem) {
@@ -180,7 +181,7 @@ struct OpsFor {
     static const Ops<T> o = {kind,     P::K,     P::NP,    P::NWS,   P::LMAX,
                              P::HAS_W, &prepare, &sweep,   &evaluate, &residual, &sweep_tma,
                              &regs, &tma_regs,
-                             WIDE,     TmaRoles<P, T, WIDE>::THREADS, &tma_occupancy, &sweep_occupancy,
+                             WIDE,     TmaRoles<P, T, WIDE>::THREADS, TmaRoles<P, T, 4>::THREADS, &tma_occupancy, &sweep_occupancy,
                              CLUSTER ? &cluster_run : nullptr, &cluster_smem, &cluster_fits};
     return &o;
   }

@@ -29,6 +29,7 @@ struct Ops {
   int (*tma_regs)(bool check);
   int wide_cw;  // consumer warps of the wide TMA sweep instantiation (8, or 4 if none)
   int wide_threads;  // threads per CTA of the wide TMA sweep (consumers + producer warp)
+  int narrow_threads;  // threads per CTA of the 4-consumer-warp TMA sweep
   // resident CTAs per SM of the plain TMA sweep at this width / shared memory
   int (*tma_occupancy)(int cw, size_t smem);
   // resident CTAs per SM of the plain register-streamed sweep

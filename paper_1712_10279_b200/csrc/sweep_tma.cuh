@@ -165,6 +165,9 @@ __device__ __forceinline__ void tma_produce(const SweepArgs<T>& A, const StageLa
 #ifndef OTFX_HEAVY_SELF
 #define OTFX_HEAVY_SELF 1
 #endif
+#ifndef OTFX_SELF_NARROW
+#define OTFX_SELF_NARROW 0
+#endif
 // Thread roles of a TMA sweep CTA: CW consumer warps plus one producer warp,
 // except (OTFX_HEAVY_SELF, default on) the wide heavy complex-Hermitian payloads, whose
 // 255-register consumers fit at most 8 warps per SM (2 per sub-partition's
@@ -173,7 +176,11 @@ __device__ __forceinline__ void tma_produce(const SweepArgs<T>& A, const StageLa
 template <class P, typename T, int CW>
 struct TmaRoles {
   static constexpr bool HEAVY = sizeof(T) == 8 && P::NCOEF == 0 && P::NP == P::K * P::K && P::K >= 3;
-  static constexpr bool SELF = OTFX_HEAVY_SELF != 0 && HEAVY && CW == 8;
+  // (OTFX_SELF_NARROW: the 2x2 complex payload's 4-warp CTAs too, so four
+  // of them fit an SM on a 2-stage ring)
+  static constexpr bool C2X2 = sizeof(T) == 8 && P::NCOEF == 0 && P::NP == P::K * P::K && P::K == 2;
+  static constexpr bool SELF = (OTFX_HEAVY_SELF != 0 && HEAVY && CW == 8) ||
+                               (OTFX_SELF_NARROW != 0 && C2X2 && CW == 4);
   static constexpr int THREADS = 32 * (CW + (SELF ? 0 : 1));
 };
 
