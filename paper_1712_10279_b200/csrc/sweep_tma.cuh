@@ -202,8 +202,13 @@ template <class P, typename T, int FL, int CWT = 4>
 // The 4-warp instantiations (matrix payloads) keep ptxas' default (0 = no
 // hint): stating minBlocks = 1 there raises the 3x3 real payload from 156 to
 // 196 registers and halves its occupancy.
+#ifndef OTFX_DUAL_MINB
+#define OTFX_DUAL_MINB 2
+#endif
 __global__ void __launch_bounds__(TmaRoles<P, T, CWT>::THREADS,
-                                  (CWT == 8 && (P::NCOEF > 0 || !P::HAS_W)) ? (FL != 0 ? 2 : 1) : 0)
+                                  (CWT == 8 && (P::NCOEF > 0 || !P::HAS_W))
+                                      ? (FL == 0 ? 1 : (FL == 2 ? OTFX_DUAL_MINB : 2))
+                                      : 0)
     sweep_tma_kernel(
     const __grid_constant__ TmaSweepArgs<T> G, const __grid_constant__ TmaSet M) {
   constexpr bool CHECK = (FL & 1) != 0;
